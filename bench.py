@@ -1,0 +1,304 @@
+#!/usr/bin/env python
+"""HER-AHALS outer iterations/s on BASELINE config 2 (300^3, r=20, FP64).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--config c2|c3|c4|c1]
+
+A "step" is one HER-AHALS outer iteration (N MTTKRPs + N fused AHALS /
+extrapolation / Gram updates + the on-device restart decision) over the full
+synthetic instance. ``value`` is device-timed (CUDA events on the session
+stream, tensor resident in HBM; the 216 MB tensor exceeds the 126 MB L2, so no
+flush is needed). ``e2e`` is the same metric through the public C-ABI driver
+ntf_her_run with host buffers: upload of the tensor and init, K iterations,
+download of factors and trace inside the timed region.
+
+``--impl reference`` times the reference algorithm's CPU implementation (the
+oracle restatement in oracle/, built with OpenMP over all host cores, because
+the reference itself cannot be compiled without Eigen3) on the same config.
+
+Multi-GPU (torchrun, one rank per GPU): the tensor is slab-sharded along
+mode 1; per-GPU work shrinks with N (strong scaling of one instance).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+CONFIGS = {
+    # name: (shape, rank, sigma, dtype, seed, BASELINE.json index)
+    "c1": ([50, 50, 50], 10, 0.01, "f64", 101, 0),
+    "c2": ([300, 300, 300], 20, 0.0, "f64", 102, 1),
+    "c3": ([100, 100, 100, 100], 16, 0.01, "f64", 103, 2),
+    "c4": ([500, 500, 500], 32, 0.01, "f32", 104, 3),
+}
+METRIC = "HER-AHALS outer iters/s"
+UNIT = "iters/s"
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh)["hbm_gbs"], "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons during the timed region."""
+
+    def __init__(self, device=0):
+        self.device = device
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def start(self):
+        def run():
+            q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap")
+            while not self._stop.is_set():
+                try:
+                    out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                         timeout=5).stdout.strip()
+                    if out:
+                        self.samples.append([x.strip() for x in out.split(",")])
+                except Exception:
+                    pass
+                self._stop.wait(0.2)
+        self._t = threading.Thread(target=run, daemon=True)
+        self._t.start()
+
+    def stop(self):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if len(s) > 3 + i and
+                          s[3 + i].lower() in ("active", "1")})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": float(self.samples[0][1]) if self.samples[0][1].replace(".", "").isdigit() else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def make_instance(P, cfg_name, rank_world=(0, 1)):
+    shape, rank, sigma, dt, seed, _ = CONFIGS[cfg_name]
+    spec = P.SyntheticSpec(shape=shape, rank=rank, noise_sigma=sigma, seed=seed)
+    t, truth = P.generate(spec, dtype=np.float32 if dt == "f32" else np.float64)
+    init = P.random_init(shape, rank, P.stream_seed(seed, 1))
+    return t, truth, init
+
+
+def cpu_reference(cfg_name, steps, warmup, sample_only=False):
+    """The reference algorithm on the host cores (oracle restatement)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle as O
+    shape, rank, sigma, dt, seed, _ = CONFIGS[cfg_name]
+    t, truth = O.generate(shape, rank, sigma, False, seed)
+    if dt == "f32":
+        t = t.astype(np.float32)
+    init = O.random_init(shape, rank, O.stream_seed(seed, 1))
+    iters = warmup + steps
+    t0 = time.perf_counter()
+    _, f0, recs = O.run("her", t, init, max_outer_iters=iters)
+    wall = time.perf_counter() - t0
+    t_start = recs[warmup - 1]["time_s"] if warmup > 0 else 0.0
+    dt_steps = recs[-1]["time_s"] - t_start
+    return steps / dt_steps, dt_steps, wall
+
+
+def run_reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cores = os.cpu_count() or 1
+    os.environ.setdefault("OMP_NUM_THREADS", str(cores))
+    rate, secs, _ = cpu_reference(args.config, args.steps, args.warmup)
+    shape, r, sigma, dt, seed, idx = CONFIGS[args.config]
+    line = {
+        "impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": dt,
+        "data": "synthetic (reference generator semantics, seeded)",
+        "config": {"workload": f"BASELINE config {idx + 1}: {'x'.join(map(str, shape))} r={r} sigma={sigma} "
+                               f"HER-AHALS", "seed": seed},
+        "cpu_baseline": {"value": rate, "unit": UNIT, "cores": int(os.environ["OMP_NUM_THREADS"]),
+                         "kind": "port",
+                         "sample": f"{args.warmup}+{args.steps} outer iterations of the full instance; the "
+                                   "reference (needs Eigen3) cannot be built, so the oracle restatement of its "
+                                   "algorithm runs (OpenMP over output rows, materialised Khatri-Rao)"},
+        "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2001_04321_b200 as P
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("gloo", init_method="env://")
+        uid = [P.Context.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        ctx = P.Context(local, rank, world, uid[0])
+    else:
+        ctx = P.Context(local)
+
+    shape, r, sigma, dt, seed, idx = CONFIGS[args.config]
+    t, truth, init = make_instance(P, args.config)
+    itemsize = 4 if dt == "f32" else 8
+    if world > 1:
+        b, e = P.slab_range(shape[0], rank, world)
+        t_local = np.ascontiguousarray(t[b:e])
+    else:
+        t_local = t
+    flags = 0
+    if args.dimtree:
+        flags |= 1
+    cfg = P.AoConfig(max_outer_iters=args.warmup + args.steps + 10**6, flags=flags)
+
+    prov = P.GpuDenseProvider(t_local, ctx, full_shape=shape)
+    sess = P.Session(prov, init, cfg, P.HerParams(), algo="her")
+    stream = torch.cuda.ExternalStream(sess.stream_ptr)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    # warm-up (also builds the CUDA graph)
+    sess.step(args.warmup)
+    sess.sync()
+    sampler = ClockSampler(local)
+    sampler.start()
+    barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    sess.step(args.steps)
+    e1.record(stream)
+    sess.sync()
+    torch.cuda.synchronize()
+    barrier()
+    clocks = sampler.stop()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        tt = torch.tensor([ms], dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    value = args.steps / (ms / 1e3)
+
+    # kernel-timing pass: CUDA events around every MTTKRP launch (direct launches)
+    sess.set_kernel_timing(True)
+    sess.step(args.steps)
+    sess.sync()
+    kms, kcnt, kernels_per_iter = sess.kernel_times()
+    sess.set_kernel_timing(False)
+    trace = sess.trace()
+    n_modes = len(shape)
+    per_mode_ms = [kms[i] / max(kcnt[i], 1) for i in range(n_modes)]
+    avg_ms = sum(kms) / max(sum(kcnt), 1)
+    local_shape = list(t_local.shape)
+    bytes_per = P.mttkrp_bytes(local_shape, r, itemsize)
+    flops_per = P.mttkrp_flops(local_shape, r)
+    hbm_peak, peak_kind = _peaks()
+    achieved_gbs = bytes_per / (avg_ms / 1e3) / 1e9
+    sess.close()
+
+    # e2e through the public C-ABI driver with host buffers
+    barrier()
+    t0 = time.perf_counter()
+    prov2 = P.GpuDenseProvider(t_local, ctx, full_shape=shape)
+    model, tr2 = P.her_run(prov2, init, P.AoConfig(max_outer_iters=args.steps, flags=flags), P.HerParams(),
+                           ctx=ctx)
+    e2e_s = time.perf_counter() - t0
+    if world > 1:
+        tt = torch.tensor([e2e_s], dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_s = float(tt.item())
+    prov2.close()
+
+    line = None
+    if rank == 0:
+        fp64_peak = 36.8  # measured DFMA TFLOP/s (profiles/fma_peaks_r01.log)
+        fp32_peak = 71.7
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            os.environ.setdefault("OMP_NUM_THREADS", str(os.cpu_count() or 1))
+            rate, secs, _ = cpu_reference(args.config, steps=args.cpu_steps, warmup=1)
+            cpu = {"value": rate, "unit": UNIT, "cores": int(os.environ["OMP_NUM_THREADS"]), "kind": "port",
+                   "sample": f"1+{args.cpu_steps} HER-AHALS outer iterations of the full instance (oracle "
+                             "restatement of the reference algorithm, OpenMP)"}
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": dt,
+            "data": "synthetic (reference generator semantics, seeded; random U[0,1) init)",
+            "config": {"workload": f"BASELINE config {idx + 1}: {'x'.join(map(str, shape))} r={r} sigma={sigma} "
+                                   f"HER-AHALS", "seed": seed, "l2": "tensor larger than L2 (no flush)",
+                       "parallelism": f"mode-1 slabs x{world}", "dimtree": bool(args.dimtree)},
+            "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm_peak, "unit": "GB/s",
+                         "frac": achieved_gbs / hbm_peak, "traffic": None, "peak_kind": peak_kind,
+                         "kernel": "MTTKRP (main kernel, avg over modes)",
+                         "bytes_per_launch": bytes_per, "avg_launch_ms": avg_ms,
+                         "per_mode_ms": per_mode_ms,
+                         "fma_tflops": flops_per / (avg_ms / 1e3) / 1e12,
+                         "fma_peak_tflops": fp32_peak if dt == "f32" else fp64_peak},
+            "e2e": {"value": args.steps / e2e_s, "unit": UNIT,
+                    "h2d_bytes_per_step": (t_local.nbytes + init.flat().nbytes) / args.steps,
+                    "d2h_bytes_per_step": (init.flat().nbytes + 64 * args.steps) / args.steps},
+            "gpu_launches": kernels_per_iter * args.steps,
+            "clocks": clocks,
+            "final_f": trace.final_f() if trace.records else None,
+            "restarts": trace.restart_count(),
+        }
+        if cpu:
+            line["cpu_baseline"] = cpu
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--dimtree", action="store_true")
+    ap.add_argument("--cpu-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference_arm(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,691 @@
+"""Python mirror of the reference toolkit's solver API for the HER-AHALS path.
+
+Names, argument meaning and error behaviour follow the reference
+(/root/reference/proj/include/ntf/*.hpp): ``AoConfig``, ``HerParams``,
+``InnerStop``, ``NnlsSolver``, ``SyntheticSpec``, ``generate``,
+``random_init``, ``stream_seed``, ``her_run``, ``ao_run``, ``RunTrace`` and the
+``ObjectiveProvider`` surface (``shape``, ``norm_sq``, ``mttkrp``) of
+``GpuDenseProvider``. Every call goes through the C ABI of libntf_b200.so;
+the compute runs in the sm_100a kernels. Exceptions map the reference's
+classes: std::invalid_argument -> ValueError (``InvalidArgument``),
+std::logic_error -> ``LogicError``, std::runtime_error -> RuntimeError.
+
+Factor models are ``KruskalModel`` objects (or plain lists) of row-major
+(I_n, r) float64 numpy arrays.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import dataclasses
+import enum
+import math
+from typing import Callable, List, Optional, Sequence
+
+import numpy as np
+
+from . import _lib as L
+
+
+# ---- errors -------------------------------------------------------------------
+
+class InvalidArgument(ValueError):
+    """std::invalid_argument in the reference."""
+
+
+class LogicError(RuntimeError):
+    """std::logic_error in the reference."""
+
+
+class CudaError(RuntimeError):
+    pass
+
+
+class NcclError(RuntimeError):
+    pass
+
+
+class UnsupportedError(RuntimeError):
+    pass
+
+
+def _err_text():
+    buf = C.create_string_buffer(2048)
+    L.lib().ntf_last_error(buf, len(buf))
+    return buf.value.decode(errors="replace")
+
+
+def _check(rc):
+    if rc == L.NTF_OK:
+        return
+    msg = _err_text()
+    cls = {L.NTF_ERR_INVALID_ARGUMENT: InvalidArgument, L.NTF_ERR_LOGIC: LogicError,
+           L.NTF_ERR_CUDA: CudaError, L.NTF_ERR_NCCL: NcclError,
+           L.NTF_ERR_UNSUPPORTED: UnsupportedError}.get(rc, RuntimeError)
+    raise cls(msg)
+
+
+def _dp(a):
+    return a.ctypes.data_as(L.dptr)
+
+
+# ---- configuration (nnls.hpp, ao.hpp, her.hpp) ----------------------------------
+
+class NnlsSolver(enum.IntEnum):
+    """include/ntf/nnls.hpp:53. Only ``ahals`` runs on the GPU path."""
+    ahals = 0
+    admm = 1
+    nesterov = 2
+    pgd = 3
+    active_set = 4
+
+
+def nnls_solver_from_name(name: str) -> NnlsSolver:
+    """src/nnls.cpp:224-231."""
+    table = {"ahals": NnlsSolver.ahals, "admm": NnlsSolver.admm, "nesterov": NnlsSolver.nesterov,
+             "pgd": NnlsSolver.pgd, "as": NnlsSolver.active_set, "active_set": NnlsSolver.active_set}
+    if name not in table:
+        raise InvalidArgument("unknown NNLS solver: " + name)
+    return table[name]
+
+
+@dataclasses.dataclass
+class InnerStop:
+    """include/ntf/nnls.hpp:20-23."""
+    max_iters: int = 50
+    rel_change_tol: float = 1e-2
+
+
+@dataclasses.dataclass
+class AoConfig:
+    """include/ntf/ao.hpp:15-24 (+ ``flags``: NTF_RUN_* performance options)."""
+    solver: NnlsSolver = NnlsSolver.ahals
+    inner_stop: InnerStop = dataclasses.field(default_factory=InnerStop)
+    max_outer_iters: int = 0
+    max_time_s: float = 0.0
+    record_factor_error: bool = False
+    ground_truth: Optional["KruskalModel"] = None
+    flags: int = 0
+
+    def validate(self):
+        """src/ao.cpp:10-15."""
+        if self.max_outer_iters <= 0 and self.max_time_s <= 0.0:
+            raise InvalidArgument("set an iteration or time budget")
+        if self.record_factor_error and self.ground_truth is None:
+            raise InvalidArgument("factor error recording needs ground truth factors")
+
+
+@dataclasses.dataclass
+class HerParams:
+    """include/ntf/her.hpp:13-21."""
+    beta0: float = 0.5
+    gamma: float = 1.05
+    gamma_bar: float = 1.01
+    eta: float = 1.5
+
+    def validate(self):
+        _check(L.lib().ntf_her_params_validate(C.byref(self._c())))
+
+    def _c(self):
+        return L.HerParamsC(self.beta0, self.gamma, self.gamma_bar, self.eta)
+
+
+@dataclasses.dataclass
+class SyntheticSpec:
+    """include/ntf/datagen.hpp:14-20 (+ ``collinear``: the build's config-4 rule)."""
+    shape: Sequence[int] = ()
+    rank: int = 1
+    noise_sigma: float = 0.0
+    ill_conditioned: bool = False
+    seed: int = 0
+    collinear: bool = False
+
+
+# ---- models and traces ----------------------------------------------------------
+
+class KruskalModel:
+    """include/ntf/kruskal.hpp:10-33: one (I_i, r) factor per mode."""
+
+    def __init__(self, factors=None):
+        self.factors: List[np.ndarray] = [np.ascontiguousarray(f, np.float64) for f in (factors or [])]
+
+    def order(self):
+        return len(self.factors)
+
+    def rank(self):
+        return self.factors[0].shape[1] if self.factors else 0
+
+    def shape(self):
+        return [f.shape[0] for f in self.factors]
+
+    def factor(self, mode):
+        return self.factors[mode]
+
+    def validate(self):
+        if not self.factors:
+            raise InvalidArgument("model must have at least one factor")
+        r = self.factors[0].shape[1]
+        if any(f.ndim != 2 or f.shape[1] != r for f in self.factors):
+            raise InvalidArgument("factor column counts disagree")
+
+    def matches_shape(self, shape):
+        return list(self.shape()) == list(shape)
+
+    def is_nonnegative(self):
+        return all(bool((f >= 0).all()) for f in self.factors)
+
+    def flat(self):
+        return np.ascontiguousarray(np.concatenate([f.ravel() for f in self.factors]))
+
+    @classmethod
+    def from_flat(cls, flat, shape, rank):
+        out, off = [], 0
+        for d in shape:
+            out.append(np.array(flat[off:off + d * rank]).reshape(d, rank))
+            off += d * rank
+        return cls(out)
+
+    def __len__(self):
+        return len(self.factors)
+
+    def __getitem__(self, i):
+        return self.factors[i]
+
+    def __iter__(self):
+        return iter(self.factors)
+
+
+def _as_model(m) -> KruskalModel:
+    return m if isinstance(m, KruskalModel) else KruskalModel(list(m))
+
+
+@dataclasses.dataclass
+class TraceRecord:
+    """include/ntf/trace.hpp:11-18."""
+    iter: int = 0
+    time_s: float = 0.0
+    f: float = 0.0
+    e: Optional[float] = None
+    restarted: Optional[bool] = None
+    beta: Optional[float] = None
+
+
+@dataclasses.dataclass
+class RunTrace:
+    """include/ntf/trace.hpp:22-37 and src/trace.cpp."""
+    f0: float = 0.0
+    records: List[TraceRecord] = dataclasses.field(default_factory=list)
+
+    def validate(self):
+        for a, b in zip(self.records, self.records[1:]):
+            if b.iter <= a.iter:
+                raise LogicError("trace iterations must strictly increase")
+            if b.time_s < a.time_s:
+                raise LogicError("trace time must not decrease")
+
+    def restart_count(self):
+        return sum(1 for r in self.records if r.restarted)
+
+    def final_f(self):
+        if not self.records:
+            raise LogicError("empty trace")
+        return self.records[-1].f
+
+    def write_csv(self, path):
+        """Schema iter,time_s,f,e,restarted,beta with %.17g (trace.cpp:43-57)."""
+        g = lambda v: "%.17g" % v  # noqa: E731
+        with open(path, "w") as fh:
+            fh.write("iter,time_s,f,e,restarted,beta\n")
+            for r in self.records:
+                fh.write(f"{r.iter},{g(r.time_s)},{g(r.f)},{'' if r.e is None else g(r.e)},"
+                         f"{'' if r.restarted is None else int(r.restarted)},"
+                         f"{'' if r.beta is None else g(r.beta)}\n")
+
+    @staticmethod
+    def read_csv(path):
+        with open(path) as fh:
+            if fh.readline().rstrip("\n") != "iter,time_s,f,e,restarted,beta":
+                raise RuntimeError(path + ": unexpected CSV header")
+            t = RunTrace()
+            for line in fh:
+                line = line.rstrip("\n")
+                if not line:
+                    continue
+                c = (line.split(",") + [""] * 6)[:6]
+                t.records.append(TraceRecord(int(c[0]), float(c[1]), float(c[2]),
+                                             float(c[3]) if c[3] else None,
+                                             (c[4] != "0") if c[4] else None,
+                                             float(c[5]) if c[5] else None))
+            return t
+
+
+@dataclasses.dataclass
+class HerIterationInfo:
+    """include/ntf/her.hpp:50-57."""
+    iter: int
+    f_hat: float
+    restarted: bool
+    beta_used: float
+    factors: KruskalModel
+    hat_factors: KruskalModel
+
+
+# ---- datagen (datagen.hpp) -------------------------------------------------------
+
+def stream_seed(base: int, stream: int) -> int:
+    """src/datagen.cpp:30-35."""
+    return int(L.lib().ntf_stream_seed(base, stream))
+
+
+def random_init(shape, rank, seed) -> KruskalModel:
+    """src/datagen.cpp:72-80."""
+    shape = [int(d) for d in shape]
+    out = np.empty(sum(shape) * rank)
+    _check(L.lib().ntf_random_init((C.c_int * len(shape))(*shape), len(shape), rank, seed, _dp(out)))
+    return KruskalModel.from_flat(out, shape, rank)
+
+
+def generate(spec: SyntheticSpec, dtype=np.float64):
+    """src/datagen.cpp:48-70 -> (tensor ndarray, truth KruskalModel)."""
+    shape = [int(d) for d in spec.shape]
+    if not shape:
+        raise InvalidArgument("tensor shape must have order >= 1")
+    dtype = np.dtype(dtype)
+    code = L.NTF_DTYPE_F32 if dtype == np.float32 else L.NTF_DTYPE_F64
+    n = 1
+    for d in shape:
+        n *= max(d, 0)
+    t = np.empty(n, dtype=np.float32 if code == L.NTF_DTYPE_F32 else np.float64)
+    truth = np.empty(max(sum(shape) * max(spec.rank, 0), 1))
+    _check(L.lib().ntf_generate((C.c_int * len(shape))(*shape), len(shape), spec.rank, spec.noise_sigma,
+                                int(spec.ill_conditioned), int(spec.collinear), spec.seed, code,
+                                t.ctypes.data_as(C.c_void_p), _dp(truth)))
+    return t.reshape(shape), KruskalModel.from_flat(truth, shape, spec.rank)
+
+
+def factor_error(est, truth) -> float:
+    """src/metrics.cpp:79-111."""
+    est, truth = _as_model(est), _as_model(truth)
+    if est.order() != truth.order() or est.rank() != truth.rank() or est.shape() != truth.shape():
+        raise InvalidArgument("factor_error: model shapes disagree")
+    shape = est.shape()
+    out = C.c_double()
+    _check(L.lib().ntf_factor_error(_dp(est.flat()), _dp(truth.flat()), (C.c_int * len(shape))(*shape),
+                                    len(shape), est.rank(), C.byref(out)))
+    return out.value
+
+
+# ---- contexts and the dense provider (provider.hpp) --------------------------------
+
+class Context:
+    """One GPU (or one rank of an NCCL world) — owns streams and the NCCL comm."""
+
+    def __init__(self, device=0, rank=0, world=1, nccl_id: Optional[bytes] = None):
+        h = C.c_void_p()
+        if world == 1:
+            _check(L.lib().ntf_ctx_create(device, C.byref(h)))
+        else:
+            if nccl_id is None or len(nccl_id) != 128:
+                raise InvalidArgument("a 128-byte NCCL unique id is required for world > 1")
+            _check(L.lib().ntf_ctx_create_dist(device, rank, world, nccl_id, C.byref(h)))
+        self.handle = h
+        self.device, self.rank, self.world = device, rank, world
+
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        _check(L.lib().ntf_nccl_unique_id(buf))
+        return buf.raw
+
+    def close(self):
+        if self.handle:
+            L.lib().ntf_ctx_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_DEFAULT_CTX = {}
+
+
+def default_context(device=0) -> Context:
+    if device not in _DEFAULT_CTX:
+        _DEFAULT_CTX[device] = Context(device)
+    return _DEFAULT_CTX[device]
+
+
+def device_count() -> int:
+    n = C.c_int()
+    _check(L.lib().ntf_device_count(C.byref(n)))
+    return n.value
+
+
+def slab_range(dim0, rank, world):
+    """Mode-1 rows [begin, end) of `rank`."""
+    b, e = C.c_int64(), C.c_int64()
+    _check(L.lib().ntf_slab_range(dim0, rank, world, C.byref(b), C.byref(e)))
+    return b.value, e.value
+
+
+class ObjectiveProvider:
+    """include/ntf/provider.hpp:14-20."""
+
+    def shape(self):
+        raise NotImplementedError
+
+    def norm_sq(self):
+        raise NotImplementedError
+
+    def mttkrp(self, model, mode):
+        raise NotImplementedError
+
+
+class GpuDenseProvider(ObjectiveProvider):
+    """DenseProvider (provider.hpp:22-34) backed by a device-resident tensor.
+
+    ``tensor``: numpy float64/float32 array holding the full tensor (or, on a
+    multi-rank context, this rank's mode-1 slab with ``full_shape`` given), or
+    a CUDA torch tensor on the context's device.
+    """
+
+    def __init__(self, tensor, ctx: Optional[Context] = None, full_shape=None):
+        self.ctx = ctx or default_context()
+        h = C.c_void_p()
+        if hasattr(tensor, "is_cuda") and tensor.is_cuda:
+            import torch  # plumbing only: the device buffer is copied into the provider
+            if tensor.dtype not in (torch.float32, torch.float64):
+                raise InvalidArgument("tensor must be float32 or float64")
+            tensor = tensor.contiguous()
+            shape = list(full_shape or tensor.shape)
+            code = L.NTF_DTYPE_F32 if tensor.dtype == torch.float32 else L.NTF_DTYPE_F64
+            arr = (C.c_int64 * len(shape))(*shape)
+            _check(L.lib().ntf_tensor_upload_device(self.ctx.handle, C.c_void_p(tensor.data_ptr()), code,
+                                                    len(shape), arr, C.byref(h)))
+        else:
+            t = np.asarray(tensor)
+            if t.dtype not in (np.float32, np.float64):
+                t = t.astype(np.float64)
+            t = np.ascontiguousarray(t)
+            shape = list(full_shape or t.shape)
+            code = L.NTF_DTYPE_F32 if t.dtype == np.float32 else L.NTF_DTYPE_F64
+            arr = (C.c_int64 * len(shape))(*shape)
+            _check(L.lib().ntf_tensor_upload(self.ctx.handle, t.ctypes.data_as(C.c_void_p), code, len(shape),
+                                             arr, C.byref(h)))
+        self.handle = h
+        self._shape = [int(d) for d in shape]
+        self.dtype = np.float32 if code == L.NTF_DTYPE_F32 else np.float64
+
+    def shape(self):
+        return list(self._shape)
+
+    def norm_sq(self):
+        out = C.c_double()
+        _check(L.lib().ntf_tensor_norm_sq(self.handle, C.byref(out)))
+        return out.value
+
+    def _model_flat(self, model):
+        m = _as_model(model)
+        m.validate()
+        if not m.matches_shape(self._shape):
+            raise InvalidArgument("mttkrp: model/tensor shape mismatch")
+        return m, m.flat()
+
+    def mttkrp(self, model, mode):
+        """provider.hpp:18 / kernels.cpp:161-191."""
+        m, flat = self._model_flat(model)
+        if not 0 <= mode < len(self._shape):
+            raise InvalidArgument("mode out of range")
+        out = np.empty((self._shape[mode], m.rank()))
+        _check(L.lib().ntf_mttkrp(self.ctx.handle, self.handle, _dp(flat), m.rank(), mode, _dp(out)))
+        return out
+
+    def objective(self, model, pivot=-1):
+        """kernels.cpp:305-311 (one MTTKRP + the cheap objective)."""
+        m, flat = self._model_flat(model)
+        out = C.c_double()
+        _check(L.lib().ntf_objective(self.ctx.handle, self.handle, _dp(flat), m.rank(), pivot, C.byref(out)))
+        return out.value
+
+    def close(self):
+        if getattr(self, "handle", None):
+            L.lib().ntf_tensor_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def solve_nnls(solver, gram, target, init, stop: Optional[InnerStop] = None, ctx: Optional[Context] = None,
+               return_sweeps=False):
+    """solve_nnls (nnls.cpp:213-222) on the GPU (AHALS only)."""
+    ctx = ctx or default_context()
+    g = np.ascontiguousarray(gram, np.float64)
+    c = np.ascontiguousarray(target, np.float64)
+    w0 = np.ascontiguousarray(init, np.float64)
+    stop = stop or InnerStop()
+    out = np.empty_like(w0)
+    sw = C.c_int()
+    _check(L.lib().ntf_solve_nnls(ctx.handle, int(solver), _dp(g), _dp(c), _dp(w0), w0.shape[0], w0.shape[1],
+                                  C.byref(L.InnerStopC(stop.max_iters, stop.rel_change_tol)), _dp(out),
+                                  C.byref(sw)))
+    return (out, sw.value) if return_sweeps else out
+
+
+def ahals_solve(gram, target, init, stop: Optional[InnerStop] = None, **kw):
+    """nnls.cpp:46-49."""
+    return solve_nnls(NnlsSolver.ahals, gram, target, init, stop, **kw)
+
+
+# ---- drivers (her.cpp / ao.cpp) ---------------------------------------------------------
+
+def _cfg_c(cfg: AoConfig, keep):
+    cfg.validate()
+    truth = None
+    if cfg.ground_truth is not None:
+        truth = _as_model(cfg.ground_truth).flat()
+        keep.append(truth)
+    c = L.AoConfigC()
+    c.solver = int(cfg.solver)
+    c.inner_stop = L.InnerStopC(cfg.inner_stop.max_iters, cfg.inner_stop.rel_change_tol)
+    c.max_outer_iters = cfg.max_outer_iters
+    c.max_time_s = cfg.max_time_s
+    c.record_factor_error = int(cfg.record_factor_error)
+    c.ground_truth = _dp(truth) if truth is not None else C.cast(None, L.dptr)
+    c.flags = cfg.flags
+    return c
+
+
+def _provider(data, ctx=None):
+    if isinstance(data, GpuDenseProvider):
+        return data
+    if isinstance(data, ObjectiveProvider):
+        raise UnsupportedError("her_run/ao_run need a GPU-resident provider (GpuDenseProvider)")
+    return GpuDenseProvider(data, ctx)
+
+
+def _records(buf, n, cap):
+    out = []
+    for i in range(min(n, cap)):
+        r = buf[i]
+        out.append(TraceRecord(r.iter, r.time_s, r.f, r.e if r.has_e else None,
+                               bool(r.restarted) if r.has_restarted else None,
+                               r.beta if r.has_beta else None))
+    return out
+
+
+def _check_inputs(p: GpuDenseProvider, init: KruskalModel, cfg: AoConfig):
+    """driver_common.hpp:14-25."""
+    cfg.validate()
+    init.validate()
+    if not init.matches_shape(p.shape()):
+        raise InvalidArgument("initial model does not match the tensor shape")
+    if not init.is_nonnegative():
+        raise InvalidArgument("initial model must be entrywise nonnegative")
+    if cfg.record_factor_error:
+        gt = _as_model(cfg.ground_truth)
+        if gt.order() != init.order() or gt.rank() != init.rank():
+            raise InvalidArgument("ground truth does not match the initial model")
+
+
+def her_run(data, init, cfg: AoConfig, params: HerParams = None,
+            observer: Optional[Callable[[HerIterationInfo], None]] = None, ctx: Optional[Context] = None):
+    """her_run (her.hpp:63-69): returns (accepted KruskalModel, RunTrace)."""
+    params = params or HerParams()
+    params.validate()
+    p = _provider(data, ctx)
+    init = _as_model(init)
+    _check_inputs(p, init, cfg)
+    keep = []
+    cc = _cfg_c(cfg, keep)
+    shape, rank = p.shape(), init.rank()
+    flat = init.flat()
+    out = np.empty_like(flat)
+    cap = cfg.max_outer_iters if cfg.max_outer_iters > 0 else 1 << 20
+    recs = (L.TraceRecordC * cap)()
+    f0 = C.c_double()
+    n = C.c_int()
+    err = []
+    tot = len(flat)
+
+    def _tramp(info_p, _user):
+        try:
+            info = info_p.contents
+            acc = KruskalModel.from_flat(np.ctypeslib.as_array(info.factors, (tot,)).copy(), shape, rank)
+            hat = KruskalModel.from_flat(np.ctypeslib.as_array(info.hat_factors, (tot,)).copy(), shape, rank)
+            observer(HerIterationInfo(info.iter, info.f_hat, bool(info.restarted), info.beta_used, acc, hat))
+        except Exception as exc:  # surfaced after the run
+            err.append(exc)
+
+    cb = L.OBSERVER(_tramp) if observer is not None else C.cast(None, L.OBSERVER)
+    _check(L.lib().ntf_her_run(p.ctx.handle, p.handle, _dp(flat), rank, C.byref(cc), C.byref(params._c()), cb,
+                               None, _dp(out), C.byref(f0), recs, cap, C.byref(n)))
+    if err:
+        raise err[0]
+    return KruskalModel.from_flat(out, shape, rank), RunTrace(f0.value, _records(recs, n.value, cap))
+
+
+def ao_run(data, init, cfg: AoConfig, ctx: Optional[Context] = None):
+    """ao_run (ao.hpp:30-33): returns (model, RunTrace)."""
+    p = _provider(data, ctx)
+    init = _as_model(init)
+    _check_inputs(p, init, cfg)
+    keep = []
+    cc = _cfg_c(cfg, keep)
+    shape, rank = p.shape(), init.rank()
+    flat = init.flat()
+    out = np.empty_like(flat)
+    cap = cfg.max_outer_iters if cfg.max_outer_iters > 0 else 1 << 20
+    recs = (L.TraceRecordC * cap)()
+    f0 = C.c_double()
+    n = C.c_int()
+    _check(L.lib().ntf_ao_run(p.ctx.handle, p.handle, _dp(flat), rank, C.byref(cc), _dp(out), C.byref(f0), recs,
+                              cap, C.byref(n)))
+    return KruskalModel.from_flat(out, shape, rank), RunTrace(f0.value, _records(recs, n.value, cap))
+
+
+# ---- HER helpers (her.cpp:16-30), host-side scalar/elementwise mirrors ---------------
+
+@dataclasses.dataclass
+class HerState:
+    """include/ntf/her.hpp:25-31 (scalar part)."""
+    beta: float = 0.0
+    beta_bar: float = 1.0
+    f_hat_prev: float = 0.0
+
+
+def update_betas(state: HerState, restarted: bool, params: HerParams):
+    """src/her.cpp:21-30 — the same arithmetic the device decision runs."""
+    if restarted:
+        state.beta_bar = state.beta
+        state.beta = state.beta / params.eta
+    else:
+        state.beta = min(state.beta_bar, state.beta * params.gamma)
+        state.beta_bar = min(1.0, state.beta_bar * params.gamma_bar)
+
+
+# ---- stepping sessions (benchmarks) -------------------------------------------------------
+
+class Session:
+    """GPU-resident her_run (algo='her') / ao_run ('ao') state after f0."""
+
+    def __init__(self, provider: GpuDenseProvider, init, cfg: AoConfig, params: HerParams = None, algo="her"):
+        init = _as_model(init)
+        _check_inputs(provider, init, cfg)
+        self._keep = []
+        cc = _cfg_c(cfg, self._keep)
+        self.provider = provider
+        self.shape, self.rank = provider.shape(), init.rank()
+        self.algo = algo
+        h = C.c_void_p()
+        params = params or HerParams()
+        _check(L.lib().ntf_session_create(provider.ctx.handle, provider.handle, 0 if algo == "her" else 1,
+                                          _dp(init.flat()), self.rank, C.byref(cc), C.byref(params._c()),
+                                          C.byref(h)))
+        self.handle = h
+
+    def step(self, iters=1):
+        _check(L.lib().ntf_session_step(self.handle, iters))
+
+    def sync(self):
+        _check(L.lib().ntf_session_sync(self.handle))
+
+    @property
+    def stream_ptr(self) -> int:
+        return int(L.lib().ntf_session_stream(self.handle) or 0)
+
+    def iterations(self):
+        n = C.c_int()
+        _check(L.lib().ntf_session_iterations(self.handle, C.byref(n)))
+        return n.value
+
+    def factors(self) -> KruskalModel:
+        out = np.empty(sum(self.shape) * self.rank)
+        _check(L.lib().ntf_session_factors(self.handle, _dp(out)))
+        return KruskalModel.from_flat(out, self.shape, self.rank)
+
+    def trace(self) -> RunTrace:
+        k = max(self.iterations(), 1)
+        recs = (L.TraceRecordC * k)()
+        f0 = C.c_double()
+        n = C.c_int()
+        _check(L.lib().ntf_session_trace(self.handle, C.byref(f0), recs, k, C.byref(n)))
+        return RunTrace(f0.value, _records(recs, n.value, k))
+
+    def set_kernel_timing(self, on=True):
+        _check(L.lib().ntf_session_set_kernel_timing(self.handle, int(on)))
+
+    def kernel_times(self):
+        """(ms summed per mode, launches per mode, kernels per outer iteration)."""
+        n = len(self.shape)
+        ms = (C.c_double * n)()
+        cnt = (C.c_int * n)()
+        tot = C.c_int()
+        _check(L.lib().ntf_session_kernel_times(self.handle, ms, cnt, C.byref(tot)))
+        return list(ms), list(cnt), tot.value
+
+    def close(self):
+        if getattr(self, "handle", None):
+            L.lib().ntf_session_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def mttkrp_bytes(shape, rank, itemsize):
+    """Algorithmic bytes of one mode-n MTTKRP, independent of n:
+    |T|*s + sum_{m != n} I_m r s + I_n r s = |T|*s + sum_m I_m r s."""
+    return math.prod(shape) * itemsize + sum(shape) * rank * itemsize
+
+
+def mttkrp_flops(shape, rank):
+    return 2 * math.prod(shape) * rank

@@ -1,0 +1,631 @@
+// extern "C" boundary (include/ntf_b200.h). Every entry point catches all
+// exceptions and maps them to status codes; messages go to a thread-local
+// buffer read by ntf_last_error().
+#include <nccl.h>
+
+#include <chrono>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "runtime.h"
+
+using namespace ntfb;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    return NTF_OK;
+  } catch (const InvalidArgument& e) {
+    g_last_error = e.what();
+    return NTF_ERR_INVALID_ARGUMENT;
+  } catch (const LogicError& e) {
+    g_last_error = e.what();
+    return NTF_ERR_LOGIC;
+  } catch (const CudaError& e) {
+    g_last_error = e.what();
+    return NTF_ERR_CUDA;
+  } catch (const NcclError& e) {
+    g_last_error = e.what();
+    return NTF_ERR_NCCL;
+  } catch (const Unsupported& e) {
+    g_last_error = e.what();
+    return NTF_ERR_UNSUPPORTED;
+  } catch (const std::invalid_argument& e) {
+    g_last_error = e.what();
+    return NTF_ERR_INVALID_ARGUMENT;
+  } catch (const std::logic_error& e) {
+    g_last_error = e.what();
+    return NTF_ERR_LOGIC;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return NTF_ERR_RUNTIME;
+  } catch (...) {
+    g_last_error = "unknown error";
+    return NTF_ERR_RUNTIME;
+  }
+}
+
+void need(const void* p, const char* what) {
+  if (!p) throw InvalidArgument(std::string(what) + " must not be null");
+}
+
+// HerParams::validate (her.cpp:10-14).
+void validate_params(const ntf_her_params& p) {
+  if (!(p.beta0 > 0.0 && p.beta0 < 1.0)) throw InvalidArgument("beta0 must lie in (0,1)");
+  if (!(1.0 < p.gamma_bar && p.gamma_bar <= p.gamma && p.gamma <= p.eta))
+    throw InvalidArgument("parameters must satisfy 1 < gamma_bar <= gamma <= eta");
+}
+
+// AoConfig::validate (ao.cpp:10-15).
+void validate_cfg(const ntf_ao_config& c) {
+  if (c.max_outer_iters <= 0 && c.max_time_s <= 0.0) throw InvalidArgument("set an iteration or time budget");
+  if (c.record_factor_error && c.ground_truth == nullptr)
+    throw InvalidArgument("factor error recording needs ground truth factors");
+}
+
+std::vector<int> int_shape(const ntf_tensor* t) {
+  std::vector<int> s(static_cast<size_t>(t->order));
+  for (int i = 0; i < t->order; ++i) s[size_t(i)] = int(t->shape[i]);
+  return s;
+}
+
+long long model_len(const ntf_tensor* t, int rank) {
+  long long n = 0;
+  for (int i = 0; i < t->order; ++i) n += t->shape[i] * rank;
+  return n;
+}
+
+// check_run_inputs (driver_common.hpp:14-25).
+void check_run_inputs(const ntf_tensor* t, const double* init, int rank, const ntf_ao_config& cfg) {
+  validate_cfg(cfg);
+  if (rank < 1) throw InvalidArgument("rank must be >= 1");
+  const long long n = model_len(t, rank);
+  for (long long e = 0; e < n; ++e)
+    if (init[e] < 0.0) throw InvalidArgument("initial model must be entrywise nonnegative");
+  if (cfg.solver != NTF_SOLVER_AHALS)
+    throw Unsupported("only the AHALS inner solver runs on the GPU path");
+  if (cfg.inner_stop.max_iters < 0) throw InvalidArgument("inner max_iters must be >= 0");
+}
+
+ntf_tensor* make_tensor(ntf_ctx* ctx, const void* src, bool src_on_device, int dtype, int order,
+                        const int64_t* shape) {
+  need(ctx, "ctx");
+  need(src, "tensor data");
+  need(shape, "shape");
+  if (dtype != NTF_DTYPE_F64 && dtype != NTF_DTYPE_F32) throw InvalidArgument("unknown dtype");
+  if (order < 1 || order > NTF_MAX_ORDER) throw InvalidArgument("tensor order must lie in 1..8");
+  auto* t = new ntf_tensor();
+  try {
+    t->ctx = ctx;
+    t->dtype = dtype;
+    t->order = order;
+    for (int i = 0; i < order; ++i) {
+      if (shape[i] < 1 || shape[i] > (1LL << 31) - 1) throw InvalidArgument("tensor dimensions must be positive");
+      t->shape[i] = shape[i];
+    }
+    long long b = 0, e = shape[0];
+    slab_range(shape[0], ctx->comm.rank, ctx->comm.world, &b, &e);
+    t->row0 = b;
+    t->rows = e - b;
+    if (t->rows < 1) throw InvalidArgument("every rank needs at least one mode-1 row");
+    t->n_local = t->rows;
+    for (int i = 1; i < order; ++i) t->n_local *= shape[i];
+    const size_t es = dtype == NTF_DTYPE_F32 ? 4 : 8;
+    NTF_CUDA(cudaSetDevice(ctx->device));
+    t->data = DevBuf(size_t(t->n_local) * es);
+    NTF_CUDA(cudaMemcpyAsync(t->data.p, src, size_t(t->n_local) * es,
+                             src_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, ctx->stream));
+    t->nsq_dev = DevBuf(sizeof(double));
+    launch_norm_sq(t->data.p, dtype, t->n_local, ctx->scratch.as<double>(), int(ctx->scratch.bytes / 8),
+                   t->nsq_dev.as<double>(), ctx->stream);
+    ctx->comm.allreduce_sum(t->nsq_dev.as<double>(), 1, ctx->stream);
+    NTF_CUDA(cudaMemcpyAsync(&t->nsq, t->nsq_dev.p, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    NTF_CUDA(cudaStreamSynchronize(ctx->stream));
+  } catch (...) {
+    delete t;
+    throw;
+  }
+  return t;
+}
+
+// A DevFactors over caller factors (sel = 0 for every mode), for the
+// per-call provider entry points.
+struct TempFactors {
+  DevBuf fac, grams, dF;
+  DevFactors h{};
+  TempFactors(const ntf_tensor* t, const double* factors, int rank, cudaStream_t s) {
+    const long long n = model_len(t, rank);
+    fac = DevBuf(size_t(n) * sizeof(double));
+    grams = DevBuf(size_t(t->order) * rank * rank * sizeof(double));
+    dF = DevBuf(sizeof(DevFactors));
+    std::memset(&h, 0, sizeof h);
+    h.order = t->order;
+    h.rank = rank;
+    long long off = 0;
+    for (int i = 0; i < t->order; ++i) {
+      h.x[i][0] = h.x[i][1] = fac.as<double>() + off;
+      h.gram[i][0] = h.gram[i][1] = grams.as<double>() + size_t(i) * rank * rank;
+      h.rows[i] = int(t->shape[i]);
+      off += t->shape[i] * rank;
+    }
+    NTF_CUDA(cudaMemcpyAsync(fac.p, factors, size_t(n) * sizeof(double), cudaMemcpyHostToDevice, s));
+    NTF_CUDA(cudaMemcpyAsync(dF.p, &h, sizeof h, cudaMemcpyHostToDevice, s));
+  }
+};
+
+void run_driver(int algo, ntf_ctx* ctx, const ntf_tensor* t, const double* init, int rank,
+                const ntf_ao_config* cfg, const ntf_her_params* params, ntf_her_observer observer, void* user,
+                double* out_factors, double* f0, ntf_trace_record* trace, int trace_cap, int* n_records) {
+  need(ctx, "ctx");
+  need(t, "tensor");
+  need(init, "init");
+  need(cfg, "config");
+  need(out_factors, "out_factors");
+  need(n_records, "n_records");
+  if (algo == 0) {
+    need(params, "params");
+    validate_params(*params);
+  }
+  check_run_inputs(t, init, rank, *cfg);
+  const auto shape = int_shape(t);
+  Session s(ctx, t, algo, init, rank, *cfg, params);
+  const long long len = model_len(t, rank);
+  const bool per_iteration = observer != nullptr || cfg->record_factor_error || cfg->max_time_s > 0.0;
+  std::vector<double> e_values;
+  if (!per_iteration) {
+    s.step(cfg->max_outer_iters);
+    s.sync();
+  } else {
+    std::vector<double> acc(static_cast<size_t>(len));
+    std::vector<ntf_trace_record> last(1);
+    while (true) {
+      s.step(1);
+      s.sync();
+      const bool finished = s.done();
+      const int k = s.iterations();
+      if (cfg->record_factor_error || observer) s.factors(acc.data());
+      if (cfg->record_factor_error)
+        e_values.push_back(factor_error(acc.data(), cfg->ground_truth, shape.data(), t->order, rank));
+      if (observer) {
+        std::vector<ntf_trace_record> all(static_cast<size_t>(k));
+        int n = 0;
+        s.trace(nullptr, all.data(), k, &n);
+        ntf_her_iteration_info info{};
+        info.iter = k;
+        info.f_hat = all[size_t(k - 1)].f;
+        info.restarted = all[size_t(k - 1)].restarted;
+        info.beta_used = all[size_t(k - 1)].beta;
+        info.factors = acc.data();
+        info.hat_factors = acc.data();  // equal after every decision (her.cpp:76-83)
+        observer(&info, user);
+      }
+      if (finished) break;
+    }
+  }
+  s.factors(out_factors);
+  std::vector<ntf_trace_record> recs(size_t(std::max(trace_cap, 0)));
+  int n = 0;
+  s.trace(f0, recs.data(), trace_cap, &n);
+  *n_records = n;
+  if (trace)
+    for (int i = 0; i < std::min(n, trace_cap); ++i) {
+      trace[i] = recs[size_t(i)];
+      if (size_t(i) < e_values.size()) {
+        trace[i].has_e = 1;
+        trace[i].e = e_values[size_t(i)];
+      }
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ntf_version(void) { return "ntf_b200 0.1 (sm_100a)"; }
+
+int ntf_last_error(char* buf, size_t n) {
+  if (buf && n) {
+    std::strncpy(buf, g_last_error.c_str(), n - 1);
+    buf[n - 1] = '\0';
+  }
+  return int(g_last_error.size());
+}
+
+void ntf_her_params_default(ntf_her_params* p) {
+  if (p) *p = ntf_her_params{0.5, 1.05, 1.01, 1.5};
+}
+
+void ntf_ao_config_default(ntf_ao_config* c) {
+  if (!c) return;
+  std::memset(c, 0, sizeof *c);
+  c->solver = NTF_SOLVER_AHALS;
+  c->inner_stop.max_iters = 50;
+  c->inner_stop.rel_change_tol = 1e-2;
+}
+
+int ntf_her_params_validate(const ntf_her_params* p) {
+  return guarded([&] {
+    need(p, "params");
+    validate_params(*p);
+  });
+}
+
+int ntf_ao_config_validate(const ntf_ao_config* c) {
+  return guarded([&] {
+    need(c, "config");
+    validate_cfg(*c);
+  });
+}
+
+uint64_t ntf_stream_seed(uint64_t base, uint64_t stream) { return stream_seed(base, stream); }
+
+int ntf_random_init(const int* shape, int order, int rank, uint64_t seed, double* out) {
+  return guarded([&] {
+    need(shape, "shape");
+    need(out, "out");
+    random_init(shape, order, rank, seed, out);
+  });
+}
+
+int ntf_generate(const int* shape, int order, int rank, double sigma, int ill_conditioned, int collinear,
+                 uint64_t seed, int dtype, void* tensor_out, double* truth_out) {
+  return guarded([&] {
+    need(shape, "shape");
+    need(tensor_out, "tensor_out");
+    need(truth_out, "truth_out");
+    generate(shape, order, rank, sigma, ill_conditioned, collinear, seed, dtype, tensor_out, truth_out);
+  });
+}
+
+int ntf_factor_error(const double* est, const double* truth, const int* shape, int order, int rank, double* out) {
+  return guarded([&] {
+    need(est, "est");
+    need(truth, "truth");
+    need(shape, "shape");
+    need(out, "out");
+    *out = factor_error(est, truth, shape, order, rank);
+  });
+}
+
+int ntf_device_count(int* n) {
+  return guarded([&] {
+    need(n, "n");
+    int c = 0;
+    const cudaError_t e = cudaGetDeviceCount(&c);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      c = 0;
+    }
+    *n = c;
+  });
+}
+
+int ntf_ctx_create(int device, ntf_ctx** out) {
+  return guarded([&] {
+    need(out, "out");
+    int n = 0;
+    NTF_CUDA(cudaGetDeviceCount(&n));
+    if (device < 0 || device >= n) throw InvalidArgument("no such CUDA device");
+    auto* c = new ntf_ctx();
+    try {
+      c->device = device;
+      NTF_CUDA(cudaSetDevice(device));
+      NTF_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+      c->sms = device_sm_count();
+      c->scratch = DevBuf(4096 * sizeof(double));
+    } catch (...) {
+      delete c;
+      throw;
+    }
+    *out = c;
+  });
+}
+
+int ntf_nccl_unique_id(unsigned char out[128]) {
+  return guarded([&] {
+    need(out, "out");
+    static_assert(sizeof(ncclUniqueId) == 128, "NCCL unique id size");
+    ncclUniqueId id;
+    const ncclResult_t r = ncclGetUniqueId(&id);
+    if (r != ncclSuccess) throw NcclError(std::string("ncclGetUniqueId: ") + ncclGetErrorString(r));
+    std::memcpy(out, &id, 128);
+  });
+}
+
+int ntf_ctx_create_dist(int device, int rank, int world, const unsigned char id[128], ntf_ctx** out) {
+  return guarded([&] {
+    need(out, "out");
+    need(id, "id");
+    if (world < 1 || rank < 0 || rank >= world) throw InvalidArgument("rank must lie in [0, world)");
+    ntf_ctx* c = nullptr;
+    const int rc = ntf_ctx_create(device, &c);
+    if (rc != NTF_OK) throw CudaError(g_last_error);
+    try {
+      c->comm.rank = rank;
+      c->comm.world = world;
+      if (world > 1) {
+        ncclUniqueId uid;
+        std::memcpy(&uid, id, 128);
+        ncclComm_t comm;
+        const ncclResult_t r = ncclCommInitRank(&comm, world, uid, rank);
+        if (r != ncclSuccess) throw NcclError(std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+        c->comm.nccl = comm;
+      }
+    } catch (...) {
+      delete c;
+      throw;
+    }
+    *out = c;
+  });
+}
+
+int ntf_ctx_info(const ntf_ctx* ctx, int* device, int* rank, int* world) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    if (device) *device = ctx->device;
+    if (rank) *rank = ctx->comm.rank;
+    if (world) *world = ctx->comm.world;
+  });
+}
+
+int ntf_ctx_destroy(ntf_ctx* ctx) {
+  return guarded([&] { delete ctx; });
+}
+
+int ntf_slab_range(int64_t dim0, int rank, int world, int64_t* begin, int64_t* end) {
+  return guarded([&] {
+    need(begin, "begin");
+    need(end, "end");
+    long long b, e;
+    slab_range(dim0, rank, world, &b, &e);
+    *begin = b;
+    *end = e;
+  });
+}
+
+int ntf_tensor_upload(ntf_ctx* ctx, const void* host, int dtype, int order, const int64_t* shape, ntf_tensor** out) {
+  return guarded([&] {
+    need(out, "out");
+    *out = make_tensor(ctx, host, false, dtype, order, shape);
+  });
+}
+
+int ntf_tensor_upload_device(ntf_ctx* ctx, const void* dev, int dtype, int order, const int64_t* shape,
+                             ntf_tensor** out) {
+  return guarded([&] {
+    need(out, "out");
+    *out = make_tensor(ctx, dev, true, dtype, order, shape);
+  });
+}
+
+int ntf_tensor_shape(const ntf_tensor* t, int* order, int64_t* shape) {
+  return guarded([&] {
+    need(t, "tensor");
+    if (order) *order = t->order;
+    if (shape)
+      for (int i = 0; i < t->order; ++i) shape[i] = t->shape[i];
+  });
+}
+
+int ntf_tensor_norm_sq(const ntf_tensor* t, double* out) {
+  return guarded([&] {
+    need(t, "tensor");
+    need(out, "out");
+    *out = t->nsq;
+  });
+}
+
+int ntf_tensor_destroy(ntf_tensor* t) {
+  return guarded([&] { delete t; });
+}
+
+int ntf_mttkrp(ntf_ctx* ctx, const ntf_tensor* t, const double* factors, int rank, int mode, double* out) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(t, "tensor");
+    need(factors, "factors");
+    need(out, "out");
+    if (rank < 1) throw InvalidArgument("rank must be >= 1");
+    if (mode < 0 || mode >= t->order) throw InvalidArgument("mode out of range");
+    NTF_CUDA(cudaSetDevice(ctx->device));
+    TempFactors tf(t, factors, rank, ctx->stream);
+    if (t->dtype == NTF_DTYPE_F32) {  // FP32 mirrors for the FP32 kernels
+      DevBuf f32(size_t(model_len(t, rank)) * sizeof(float));
+      long long off = 0;
+      for (int i = 0; i < t->order; ++i) {
+        tf.h.x32[i][0] = tf.h.x32[i][1] = f32.as<float>() + off;
+        off += t->shape[i] * rank;
+      }
+      NTF_CUDA(cudaMemcpyAsync(tf.dF.p, &tf.h, sizeof tf.h, cudaMemcpyHostToDevice, ctx->stream));
+      launch_init_factors(tf.dF.as<DevFactors>(), tf.h, ctx->stream);
+      MttkrpEngine eng(ctx, t, rank, 0);
+      DevBuf C(size_t(t->shape[mode]) * rank * sizeof(double));
+      eng.run(mode, tf.dF.as<DevFactors>(), C.as<double>(), ctx->stream);
+      NTF_CUDA(cudaMemcpyAsync(out, C.p, C.bytes, cudaMemcpyDeviceToHost, ctx->stream));
+      NTF_CUDA(cudaStreamSynchronize(ctx->stream));
+      return;
+    }
+    MttkrpEngine eng(ctx, t, rank, 0);
+    DevBuf C(size_t(t->shape[mode]) * rank * sizeof(double));
+    eng.run(mode, tf.dF.as<DevFactors>(), C.as<double>(), ctx->stream);
+    NTF_CUDA(cudaMemcpyAsync(out, C.p, C.bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    NTF_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int ntf_objective(ntf_ctx* ctx, const ntf_tensor* t, const double* factors, int rank, int pivot, double* out) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(t, "tensor");
+    need(factors, "factors");
+    need(out, "out");
+    if (rank < 1) throw InvalidArgument("rank must be >= 1");
+    const int p = pivot < 0 ? t->order - 1 : pivot;
+    if (p >= t->order) throw InvalidArgument("mode out of range");
+    NTF_CUDA(cudaSetDevice(ctx->device));
+    TempFactors tf(t, factors, rank, ctx->stream);
+    DevBuf f32;
+    if (t->dtype == NTF_DTYPE_F32) {
+      f32 = DevBuf(size_t(model_len(t, rank)) * sizeof(float));
+      long long off = 0;
+      for (int i = 0; i < t->order; ++i) {
+        tf.h.x32[i][0] = tf.h.x32[i][1] = f32.as<float>() + off;
+        off += t->shape[i] * rank;
+      }
+      NTF_CUDA(cudaMemcpyAsync(tf.dF.p, &tf.h, sizeof tf.h, cudaMemcpyHostToDevice, ctx->stream));
+    }
+    launch_init_factors(tf.dF.as<DevFactors>(), tf.h, ctx->stream);
+    MttkrpEngine eng(ctx, t, rank, 0);
+    DevBuf C(size_t(t->shape[p]) * rank * sizeof(double));
+    DevBuf res(sizeof(double));
+    eng.run(p, tf.dF.as<DevFactors>(), C.as<double>(), ctx->stream);
+    launch_objective(tf.dF.as<DevFactors>(), t->order, rank, p, int(t->shape[p]), C.as<double>(),
+                     t->nsq_dev.as<double>(), res.as<double>(), ctx->stream);
+    NTF_CUDA(cudaMemcpyAsync(out, res.p, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    NTF_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int ntf_solve_nnls(ntf_ctx* ctx, int solver, const double* gram, const double* target, const double* init,
+                   int rows, int rank, const ntf_inner_stop* stop, double* out, int* sweeps) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(gram, "gram");
+    need(target, "target");
+    need(init, "init");
+    need(out, "out");
+    if (solver != NTF_SOLVER_AHALS) throw Unsupported("only the AHALS inner solver runs on the GPU path");
+    if (rows < 1 || rank < 1) throw InvalidArgument("rows and rank must be >= 1");
+    const ntf_inner_stop st = stop ? *stop : ntf_inner_stop{50, 1e-2};
+    NTF_CUDA(cudaSetDevice(ctx->device));
+    const size_t n = size_t(rows) * rank;
+    DevBuf g(size_t(rank) * rank * 8), c(n * 8), w0(n * 8), w(n * 8), sw(sizeof(int));
+    DevBuf scratch(size_t(3072 + 64 * kMaxRank * kMaxRank) * sizeof(double));
+    NTF_CUDA(cudaMemcpyAsync(g.p, gram, g.bytes, cudaMemcpyHostToDevice, ctx->stream));
+    NTF_CUDA(cudaMemcpyAsync(c.p, target, n * 8, cudaMemcpyHostToDevice, ctx->stream));
+    NTF_CUDA(cudaMemcpyAsync(w0.p, init, n * 8, cudaMemcpyHostToDevice, ctx->stream));
+    NnlsLaunch a{};
+    a.rows = rows;
+    a.rank = rank;
+    a.role = 2;
+    a.C = c.as<double>();
+    a.gram_in = g.as<double>();
+    a.w0 = w0.as<double>();
+    a.w_out = w.as<double>();
+    a.sweeps_out = sw.as<int>();
+    a.max_iters = st.max_iters;
+    a.tol = st.rel_change_tol;
+    a.scratch = scratch.as<double>();
+    launch_nnls(a, ctx->stream);
+    int s = 0;
+    NTF_CUDA(cudaMemcpyAsync(out, w.p, n * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    NTF_CUDA(cudaMemcpyAsync(&s, sw.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    NTF_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (sweeps) *sweeps = s;
+  });
+}
+
+int ntf_her_run(ntf_ctx* ctx, const ntf_tensor* t, const double* init, int rank, const ntf_ao_config* cfg,
+                const ntf_her_params* params, ntf_her_observer observer, void* user, double* out_factors,
+                double* f0, ntf_trace_record* trace, int trace_cap, int* n_records) {
+  return guarded([&] {
+    run_driver(0, ctx, t, init, rank, cfg, params, observer, user, out_factors, f0, trace, trace_cap, n_records);
+  });
+}
+
+int ntf_ao_run(ntf_ctx* ctx, const ntf_tensor* t, const double* init, int rank, const ntf_ao_config* cfg,
+               double* out_factors, double* f0, ntf_trace_record* trace, int trace_cap, int* n_records) {
+  return guarded([&] {
+    run_driver(1, ctx, t, init, rank, cfg, nullptr, nullptr, nullptr, out_factors, f0, trace, trace_cap,
+               n_records);
+  });
+}
+
+int ntf_session_create(ntf_ctx* ctx, const ntf_tensor* t, int algo, const double* init, int rank,
+                       const ntf_ao_config* cfg, const ntf_her_params* params, ntf_session** out) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(t, "tensor");
+    need(init, "init");
+    need(cfg, "config");
+    need(out, "out");
+    if (algo != 0 && algo != 1) throw InvalidArgument("algo must be 0 (HER) or 1 (AO)");
+    if (algo == 0) {
+      need(params, "params");
+      validate_params(*params);
+    }
+    check_run_inputs(t, init, rank, *cfg);
+    *out = reinterpret_cast<ntf_session*>(new Session(ctx, t, algo, init, rank, *cfg, params));
+  });
+}
+
+#define SESSION(s) reinterpret_cast<Session*>(s)
+
+int ntf_session_step(ntf_session* s, int iters) {
+  return guarded([&] {
+    need(s, "session");
+    SESSION(s)->step(iters);
+  });
+}
+
+int ntf_session_sync(ntf_session* s) {
+  return guarded([&] {
+    need(s, "session");
+    SESSION(s)->sync();
+  });
+}
+
+void* ntf_session_stream(ntf_session* s) { return s ? static_cast<void*>(SESSION(s)->stream()) : nullptr; }
+
+int ntf_session_iterations(ntf_session* s, int* done) {
+  return guarded([&] {
+    need(s, "session");
+    need(done, "done");
+    *done = SESSION(s)->iterations();
+  });
+}
+
+int ntf_session_factors(ntf_session* s, double* out) {
+  return guarded([&] {
+    need(s, "session");
+    need(out, "out");
+    SESSION(s)->factors(out);
+  });
+}
+
+int ntf_session_trace(ntf_session* s, double* f0, ntf_trace_record* trace, int cap, int* n) {
+  return guarded([&] {
+    need(s, "session");
+    need(n, "n");
+    std::vector<ntf_trace_record> tmp(size_t(std::max(cap, 0)));
+    SESSION(s)->trace(f0, tmp.data(), cap, n);
+    if (trace)
+      for (int i = 0; i < std::min(*n, cap); ++i) trace[i] = tmp[size_t(i)];
+  });
+}
+
+int ntf_session_set_kernel_timing(ntf_session* s, int on) {
+  return guarded([&] {
+    need(s, "session");
+    SESSION(s)->set_kernel_timing(on != 0);
+  });
+}
+
+int ntf_session_kernel_times(ntf_session* s, double* ms_per_mode, int* launches_per_mode, int* total) {
+  return guarded([&] {
+    need(s, "session");
+    SESSION(s)->kernel_times(ms_per_mode, launches_per_mode, total);
+  });
+}
+
+int ntf_session_destroy(ntf_session* s) {
+  return guarded([&] { delete SESSION(s); });
+}
+
+}  // extern "C"

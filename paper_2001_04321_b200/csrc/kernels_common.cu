@@ -1,0 +1,265 @@
+// Generic MTTKRP, deterministic reductions, Grams and the cheap objective.
+//
+// Determinism contract (README.md:155-157 of the reference): every value is
+// produced by a fixed accumulation order that depends only on the shapes and
+// the launch configuration, never on scheduling — no floating-point atomics.
+#include <cstdio>
+
+#include "ntf_internal.h"
+
+namespace ntfb {
+
+void cuda_fail(cudaError_t e, const char* what, const char* file, int line) {
+  char buf[512];
+  snprintf(buf, sizeof buf, "CUDA error %s (%s) at %s:%d: %s", cudaGetErrorName(e), cudaGetErrorString(e),
+           file, line, what);
+  throw CudaError(buf);
+}
+
+int device_sm_count() {
+  int dev = 0, n = 0;
+  NTF_CUDA(cudaGetDevice(&dev));
+  NTF_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
+  return n;
+}
+
+namespace {
+
+constexpr int kGenThreads = 256;
+constexpr int kGenCols = 8;
+
+// Fixed-shape tree reduction of kGenThreads values per column.
+__device__ __forceinline__ void block_tree_sum(double (&acc)[kGenCols], double* sm) {
+  const int t = threadIdx.x;
+#pragma unroll
+  for (int c = 0; c < kGenCols; ++c) sm[c * kGenThreads + t] = acc[c];
+  __syncthreads();
+  for (int half = kGenThreads / 2; half > 0; half >>= 1) {
+    if (t < half) {
+#pragma unroll
+      for (int c = 0; c < kGenCols; ++c) sm[c * kGenThreads + t] += sm[c * kGenThreads + t + half];
+    }
+    __syncthreads();
+  }
+}
+
+// One block per (output row, segment of the (left,right) plane, 8-column
+// group). Each element contributes T * prod_{l != mode} A_l[i_l, c]
+// (kernels.cpp:161-191, without materialising the Khatri-Rao rows).
+template <typename T>
+__global__ void __launch_bounds__(kGenThreads)
+    mttkrp_generic_kernel(const T* __restrict__ t, ModeView v, const DevFactors* __restrict__ F,
+                          double* __restrict__ partial, long long seg_len) {
+  __shared__ double sm[kGenCols * kGenThreads];
+  const long long mid = blockIdx.x;
+  const long long seg = blockIdx.y;
+  const int c0 = blockIdx.z * kGenCols;
+  const int r = v.rank;
+  const long long plane = v.L * v.R;
+  const long long e0 = seg * seg_len;
+  const long long e1 = min(plane, e0 + seg_len);
+  const double* A[kMaxOrder];
+  for (int l = 0; l < v.order; ++l) A[l] = F->x[l][F->sel[l]];
+
+  double acc[kGenCols];
+#pragma unroll
+  for (int c = 0; c < kGenCols; ++c) acc[c] = 0.0;
+  for (long long e = e0 + threadIdx.x; e < e1; e += kGenThreads) {
+    const long long left = e / v.R;
+    const long long right = e - left * v.R;
+    const double tv = double(t[(left * v.I + mid) * v.R + right]);
+    int idx[kMaxOrder];
+    long long rem = right;
+    for (int l = v.order - 1; l > v.mode; --l) {
+      idx[l] = int(rem % v.dims[l]);
+      rem /= v.dims[l];
+    }
+    rem = left;
+    for (int l = v.mode - 1; l >= 0; --l) {
+      idx[l] = int(rem % v.dims[l]);
+      rem /= v.dims[l];
+    }
+    if (v.mode != 0) idx[0] += int(v.row0);  // slab rows index the full A_1
+#pragma unroll
+    for (int c = 0; c < kGenCols; ++c) {
+      if (c0 + c < r) {
+        double w = tv;
+        for (int l = 0; l < v.order; ++l)
+          if (l != v.mode) w *= A[l][(long long)idx[l] * r + c0 + c];
+        acc[c] += w;
+      }
+    }
+  }
+  block_tree_sum(acc, sm);
+  if (threadIdx.x < kGenCols && c0 + threadIdx.x < r)
+    partial[(seg * v.I + mid) * r + c0 + threadIdx.x] = sm[threadIdx.x * kGenThreads];
+}
+
+__global__ void reduce_partials_kernel(const double* __restrict__ partial, int segs, long long n,
+                                       double* __restrict__ out) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int k = 0; k < segs; ++k) s += partial[k * n + i];
+    out[i] = s;
+  }
+}
+
+constexpr int kNormBlocks = 592;  // fixed, so the sum order is device-independent
+
+template <typename T>
+__global__ void __launch_bounds__(256) norm_sq_kernel(const T* __restrict__ t, long long n,
+                                                      double* __restrict__ scratch) {
+  __shared__ double sm[256];
+  double s = 0.0;
+  for (long long i = blockIdx.x * 256LL + threadIdx.x; i < n; i += 256LL * kNormBlocks) {
+    const double x = double(t[i]);
+    s += x * x;
+  }
+  sm[threadIdx.x] = s;
+  __syncthreads();
+  for (int half = 128; half > 0; half >>= 1) {
+    if (threadIdx.x < half) sm[threadIdx.x] += sm[threadIdx.x + half];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) scratch[blockIdx.x] = sm[0];
+}
+
+__global__ void sum_scratch_kernel(const double* __restrict__ scratch, int n, double* __restrict__ out) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    double s = 0.0;
+    for (int i = 0; i < n; ++i) s += scratch[i];
+    *out = s;
+  }
+}
+
+// Gram of one row-major rows x r matrix, ascending-row order per entry.
+__device__ void gram_rows(const double* __restrict__ a, int rows, int r, double* __restrict__ g) {
+  for (int e = threadIdx.x; e < r * r; e += blockDim.x) {
+    const int p = e / r, q = e % r;
+    double s = 0.0;
+    for (int i = 0; i < rows; ++i) s += a[(long long)i * r + p] * a[(long long)i * r + q];
+    g[e] = s;
+  }
+}
+
+// Grams of the X-role buffers plus the FP32 mirrors of both buffers.
+__global__ void init_factors_kernel(DevFactors* F) {
+  const int mode = blockIdx.x;
+  const int rows = F->rows[mode], r = F->rank;
+  const int b = F->sel[mode];
+  gram_rows(F->x[mode][b], rows, r, F->gram[mode][b]);
+  for (int bb = 0; bb < 2; ++bb) {
+    float* m = F->x32[mode][bb];
+    const double* x = F->x[mode][bb];
+    if (m && x)
+      for (long long e = threadIdx.x; e < (long long)rows * r; e += blockDim.x) m[e] = float(x[e]);
+  }
+}
+
+// cheap_objective at `pivot` (kernels.cpp:298-303 with the pivot of :305-311).
+__global__ void __launch_bounds__(256) objective_kernel(const DevFactors* __restrict__ F, int order, int r,
+                                                        int pivot, int rows, const double* __restrict__ C,
+                                                        const double* __restrict__ nsq,
+                                                        double* __restrict__ out) {
+  extern __shared__ double sm[];  // ga[r*r], red[256]
+  double* ga = sm;
+  double* red = sm + r * r;
+  const double* a = F->x[pivot][F->sel[pivot]];
+  gram_rows(a, rows, r, ga);
+  double cross = 0.0;
+  for (long long e = threadIdx.x; e < (long long)rows * r; e += blockDim.x) cross += a[e] * C[e];
+  red[threadIdx.x] = cross;
+  __syncthreads();
+  for (int half = 128; half > 0; half >>= 1) {
+    if (threadIdx.x < half) red[threadIdx.x] += red[threadIdx.x + half];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    double quad = 0.0;
+    for (int e = 0; e < r * r; ++e) {
+      double g = 1.0;
+      for (int j = 0; j < order; ++j)
+        if (j != pivot) g *= F->gram[j][F->sel[j]][e];
+      quad += ga[e] * g;
+    }
+    *out = 0.5 * (*nsq) - red[0] + 0.5 * quad;
+  }
+}
+
+__global__ void stamp_start_kernel(RunState* st) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  st->t_start_ns = t;
+}
+
+__global__ void compact_rows_kernel(const double* __restrict__ gathered, long long maxrows,
+                                    const long long* __restrict__ begins, const long long* __restrict__ counts,
+                                    int world, int r, double* __restrict__ out) {
+  for (int p = 0; p < world; ++p) {
+    const long long n = counts[p] * r;
+    const double* src = gathered + (long long)p * maxrows * r;
+    double* dst = out + begins[p] * r;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n;
+         e += (long long)gridDim.x * blockDim.x)
+      dst[e] = src[e];
+  }
+}
+
+}  // namespace
+
+void launch_mttkrp_generic(const void* t, int dtype, const ModeView& v, const DevFactors* dF, double* partial,
+                           int segs, cudaStream_t s) {
+  const long long plane = v.L * v.R;
+  const long long seg_len = (plane + segs - 1) / segs;
+  dim3 grid(unsigned(v.I), unsigned(segs), unsigned((v.rank + kGenCols - 1) / kGenCols));
+  if (dtype == NTF_DTYPE_F32)
+    mttkrp_generic_kernel<float><<<grid, kGenThreads, 0, s>>>(static_cast<const float*>(t), v, dF, partial, seg_len);
+  else
+    mttkrp_generic_kernel<double><<<grid, kGenThreads, 0, s>>>(static_cast<const double*>(t), v, dF, partial,
+                                                               seg_len);
+  NTF_CUDA(cudaGetLastError());
+}
+
+void launch_reduce_partials(const double* partial, int segs, long long n, double* out, cudaStream_t s) {
+  const int threads = 256;
+  const long long blocks = std::min<long long>((n + threads - 1) / threads, 4096);
+  reduce_partials_kernel<<<unsigned(blocks), threads, 0, s>>>(partial, segs, n, out);
+  NTF_CUDA(cudaGetLastError());
+}
+
+void launch_norm_sq(const void* t, int dtype, long long n, double* scratch, int scratch_len, double* out,
+                    cudaStream_t s) {
+  if (scratch_len < kNormBlocks) throw LogicError("norm_sq scratch too small");
+  if (dtype == NTF_DTYPE_F32)
+    norm_sq_kernel<float><<<kNormBlocks, 256, 0, s>>>(static_cast<const float*>(t), n, scratch);
+  else
+    norm_sq_kernel<double><<<kNormBlocks, 256, 0, s>>>(static_cast<const double*>(t), n, scratch);
+  sum_scratch_kernel<<<1, 32, 0, s>>>(scratch, kNormBlocks, out);
+  NTF_CUDA(cudaGetLastError());
+}
+
+void launch_init_factors(DevFactors* dF, const DevFactors& hF, cudaStream_t s) {
+  init_factors_kernel<<<hF.order, 256, 0, s>>>(dF);
+  NTF_CUDA(cudaGetLastError());
+}
+
+void launch_objective(const DevFactors* dF, int order, int rank, int pivot, int rows, const double* C,
+                      const double* nsq_dev, double* out, cudaStream_t s) {
+  const size_t smem = sizeof(double) * (size_t(rank) * rank + 256);
+  objective_kernel<<<1, 256, smem, s>>>(dF, order, rank, pivot, rows, C, nsq_dev, out);
+  NTF_CUDA(cudaGetLastError());
+}
+
+void launch_stamp_start(RunState* st, cudaStream_t s) {
+  stamp_start_kernel<<<1, 1, 0, s>>>(st);
+  NTF_CUDA(cudaGetLastError());
+}
+
+void launch_compact_rows(const double* gathered, long long maxrows, const long long* begins,
+                         const long long* counts, int world, int r, double* out, cudaStream_t s) {
+  compact_rows_kernel<<<64, 256, 0, s>>>(gathered, maxrows, begins, counts, world, r, out);
+  NTF_CUDA(cudaGetLastError());
+}
+
+}  // namespace ntfb

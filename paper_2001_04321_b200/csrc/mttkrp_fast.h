@@ -1,0 +1,19 @@
+// Fast sm_100a MTTKRP paths (TMA-staged tensor tiles, on-the-fly Khatri-Rao
+// rows, register-blocked CUDA-core FMA, deterministic split-K reduction).
+#pragma once
+
+#include "ntf_internal.h"
+
+namespace ntfb {
+
+// True when the view/dtype/rank has a fast kernel on this build.
+bool fast_mttkrp_supported(const ModeView& v, int dtype);
+// Kernel launches per MTTKRP call on the fast path.
+int fast_mttkrp_kernels(const ModeView& v, int dtype);
+// Doubles of split-K workspace the fast path needs for this view.
+size_t fast_mttkrp_partial_len(const ModeView& v, int dtype, int sms);
+// out = MTTKRP (I x r, FP64) of the local view.
+void fast_mttkrp(const void* t, int dtype, const ModeView& v, const DevFactors* dF, double* partial, double* out,
+                 int sms, cudaStream_t s);
+
+}  // namespace ntfb

@@ -1,0 +1,128 @@
+// Internal declarations shared by the CUDA kernels and the host runtime of
+// libntf_b200.so. Nothing here crosses the C ABI (include/ntf_b200.h).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+#include "../../include/ntf_b200.h"
+
+namespace ntfb {
+
+constexpr int kMaxOrder = NTF_MAX_ORDER;
+constexpr int kMaxRank = 64;  // largest r served by the fused NNLS kernel
+
+// ---- errors ----------------------------------------------------------------
+// Host code throws these; the C ABI maps them to status codes.
+struct InvalidArgument : std::invalid_argument {
+  using std::invalid_argument::invalid_argument;
+};
+struct LogicError : std::logic_error {
+  using std::logic_error::logic_error;
+};
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct NcclError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct Unsupported : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+void cuda_fail(cudaError_t e, const char* what, const char* file, int line);
+#define NTF_CUDA(x)                                                   \
+  do {                                                                \
+    cudaError_t e__ = (x);                                            \
+    if (e__ != cudaSuccess) ::ntfb::cuda_fail(e__, #x, __FILE__, __LINE__); \
+  } while (0)
+
+// ---- device-resident solver state ------------------------------------------
+// Two FP64 buffers per mode. Role X_i = x[i][sel[i]] holds the accepted
+// factor (== the extrapolated twin at the start of an outer iteration);
+// role S_i = x[i][sel[i]^1] receives the NNLS solution. A restart flips sel
+// (X := S for every mode) instead of copying (her.cpp:76-80). gram[i][b] is
+// always the Gram of buffer x[i][b]; x32 are FP32 mirrors for FP32 tensors.
+struct DevFactors {
+  double* x[kMaxOrder][2];
+  float* x32[kMaxOrder][2];
+  double* gram[kMaxOrder][2];
+  int sel[kMaxOrder];
+  int rows[kMaxOrder];
+  int order, rank;
+};
+
+// HER/AO scalars (her.hpp:25-31) plus run bookkeeping, all on the device.
+struct RunState {
+  double beta, beta_bar, f_prev, f_last, f0, nsq;
+  double beta0, gamma, gamma_bar, eta;
+  double max_time_s;
+  double tol;
+  unsigned long long t_start_ns;
+  int k, done, max_iters, inner_max_iters;
+  int algo;  // 0 = HER, 1 = AO
+  int last_sweeps[kMaxOrder];
+};
+
+struct TraceEntry {
+  double f, beta, time_s;
+  int restarted, pad;
+};
+
+// Mode view (L, I, R) of the LOCAL slab (kernels.cpp:10-27); dims[0] is the
+// local slab height and row0 its offset in the full mode-1 factor.
+struct ModeView {
+  int order, mode, rank;
+  int dims[kMaxOrder];
+  long long L, I, R;
+  long long row0;
+};
+
+// ---- kernel launchers (CUDA translation units) ------------------------------
+struct MttkrpPlan;
+
+// Generic MTTKRP (any shape / rank): partial[seg][I][r] in FP64.
+void launch_mttkrp_generic(const void* t, int dtype, const ModeView& v, const DevFactors* dF,
+                           double* partial, int segs, cudaStream_t s);
+// Deterministic fixed-order sum of `segs` partial slabs of n values.
+void launch_reduce_partials(const double* partial, int segs, long long n, double* out, cudaStream_t s);
+// Fixed-order FP64 sum of squares of a device array.
+void launch_norm_sq(const void* t, int dtype, long long n, double* scratch, int scratch_len, double* out,
+                    cudaStream_t s);
+// gram[i][b] = x[i][b]^T x[i][b] for every mode (b = sel) and FP32 mirrors.
+void launch_init_factors(DevFactors* dF, const DevFactors& hF, cudaStream_t s);
+// cheap objective at pivot: 0.5 nsq - <A,C> + 0.5 <A^T A, G>, G = hadamard of
+// the X-role Grams except `pivot` (kernels.cpp:298-311). Writes *out.
+void launch_objective(const DevFactors* dF, int order, int rank, int pivot, int rows, const double* C,
+                      const double* nsq_dev, double* out, cudaStream_t s);
+void launch_stamp_start(RunState* st, cudaStream_t s);
+void launch_compact_rows(const double* gathered, long long maxrows, const long long* begins,
+                         const long long* counts, int world, int rank_cols, double* out, cudaStream_t s);
+
+// Fused AHALS + extrapolate/project + Grams + objective/decision kernel.
+struct NnlsLaunch {
+  int mode, order, rows, rank;
+  int role;  // 0 = HER driver, 1 = AO driver, 2 = standalone solve
+  int last;  // mode == order-1 in a driver
+  const double* C;
+  DevFactors* F;      // drivers
+  RunState* st;       // drivers
+  TraceEntry* trace;  // drivers
+  // standalone solve
+  const double* gram_in;
+  const double* w0;
+  double* w_out;
+  int* sweeps_out;
+  int max_iters;
+  double tol;
+  double* scratch;  // >= grid * (kMaxRank*kMaxRank + 64) doubles
+  unsigned int* counter;
+};
+void launch_nnls(const NnlsLaunch& a, cudaStream_t s);
+
+int device_sm_count();
+
+}  // namespace ntfb

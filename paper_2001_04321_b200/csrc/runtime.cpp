@@ -1,0 +1,391 @@
+// Host runtime: device buffers, NCCL plumbing, the MTTKRP engine and the
+// GPU-resident HER / AO sessions.
+#include "runtime.h"
+
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstring>
+#include <string>
+
+#include "mttkrp_fast.h"
+
+namespace ntfb {
+
+// ---- DevBuf ------------------------------------------------------------------
+DevBuf::DevBuf(size_t n) : bytes(n) {
+  if (n) NTF_CUDA(cudaMalloc(&p, n));
+}
+DevBuf::~DevBuf() {
+  if (p) cudaFree(p);
+}
+DevBuf& DevBuf::operator=(DevBuf&& o) noexcept {
+  if (this != &o) {
+    if (p) cudaFree(p);
+    p = o.p;
+    bytes = o.bytes;
+    o.p = nullptr;
+    o.bytes = 0;
+  }
+  return *this;
+}
+
+// ---- NCCL ----------------------------------------------------------------------
+static void nccl_check(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess) throw NcclError(std::string("NCCL failure in ") + what + ": " + ncclGetErrorString(r));
+}
+
+void Comm::allreduce_sum(double* buf, size_t n, cudaStream_t s) const {
+  if (world == 1) return;
+  nccl_check(ncclAllReduce(buf, buf, n, ncclDouble, ncclSum, static_cast<ncclComm_t>(nccl), s), "ncclAllReduce");
+}
+
+void Comm::allgather(double* buf, size_t n_per_rank, cudaStream_t s) const {
+  if (world == 1) return;
+  nccl_check(ncclAllGather(buf + size_t(rank) * n_per_rank, buf, n_per_rank, ncclDouble,
+                           static_cast<ncclComm_t>(nccl), s),
+             "ncclAllGather");
+}
+
+Comm::~Comm() {
+  if (nccl) ncclCommDestroy(static_cast<ncclComm_t>(nccl));
+}
+
+void slab_range(long long dim0, int rank, int world, long long* begin, long long* end) {
+  if (world < 1 || rank < 0 || rank >= world) throw InvalidArgument("rank must lie in [0, world)");
+  if (dim0 < 1) throw InvalidArgument("tensor dimensions must be positive");
+  const long long base = dim0 / world, extra = dim0 % world;
+  const long long b = rank < extra ? rank * (base + 1) : extra * (base + 1) + (rank - extra) * base;
+  *begin = b;
+  *end = b + base + (rank < extra ? 1 : 0);
+}
+
+// ---- MTTKRP engine -------------------------------------------------------------
+ModeView MttkrpEngine::view(int mode) const {
+  ModeView v{};
+  v.order = t_->order;
+  v.mode = mode;
+  v.rank = rank_;
+  for (int l = 0; l < t_->order; ++l) v.dims[l] = int(l == 0 ? t_->rows : t_->shape[l]);
+  v.L = 1;
+  v.R = 1;
+  for (int l = 0; l < mode; ++l) v.L *= v.dims[l];
+  v.I = v.dims[mode];
+  for (int l = mode + 1; l < t_->order; ++l) v.R *= v.dims[l];
+  v.row0 = t_->row0;
+  return v;
+}
+
+MttkrpEngine::MttkrpEngine(const ntf_ctx* ctx, const ntf_tensor* t, int rank, unsigned flags)
+    : ctx_(ctx), t_(t), rank_(rank), flags_(flags) {
+  size_t need = 0;
+  for (int m = 0; m < t->order; ++m) {
+    const ModeView v = view(m);
+    const long long cgroups = (rank + 7) / 8;
+    const long long plane = v.L * v.R;
+    long long segs = (4LL * ctx->sms + v.I * cgroups - 1) / (v.I * cgroups);
+    segs = std::max(1LL, std::min({segs, std::max(1LL, plane / 256), 1024LL}));
+    segs_[m] = int(segs);
+    need = std::max(need, size_t(segs) * size_t(v.I) * rank);
+    need = std::max(need, fast_mttkrp_partial_len(v, t->dtype, ctx->sms));
+  }
+  partial_ = DevBuf(need * sizeof(double));
+  if (ctx->comm.world > 1) {
+    const int world = ctx->comm.world;
+    std::vector<long long> meta(static_cast<size_t>(2 * world));
+    for (int p = 0; p < world; ++p) {
+      long long b, e;
+      slab_range(t->shape[0], p, world, &b, &e);
+      meta[size_t(p)] = b;
+      meta[size_t(world + p)] = e - b;
+      maxrows_ = std::max(maxrows_, e - b);
+    }
+    gather_ = DevBuf(size_t(maxrows_) * world * rank * sizeof(double));
+    slab_meta_ = DevBuf(meta.size() * sizeof(long long));
+    NTF_CUDA(cudaMemcpy(slab_meta_.p, meta.data(), meta.size() * sizeof(long long), cudaMemcpyHostToDevice));
+  }
+}
+
+int MttkrpEngine::kernels_per_call(int mode) const {
+  const ModeView v = view(mode);
+  if (!(flags_ & NTF_RUN_GENERIC) && fast_mttkrp_supported(v, t_->dtype)) return fast_mttkrp_kernels(v, t_->dtype);
+  return 2;
+}
+
+void MttkrpEngine::run(int mode, const DevFactors* dF, double* out, cudaStream_t s, cudaEvent_t ev0,
+                       cudaEvent_t ev1) {
+  const ModeView v = view(mode);
+  const Comm& comm = ctx_->comm;
+  const bool gather = comm.world > 1 && mode == 0;
+  double* dst = gather ? gather_.as<double>() + size_t(comm.rank) * maxrows_ * rank_ : out;
+  if (ev0) NTF_CUDA(cudaEventRecord(ev0, s));
+  if (!(flags_ & NTF_RUN_GENERIC) && fast_mttkrp_supported(v, t_->dtype)) {
+    fast_mttkrp(t_->data.p, t_->dtype, v, dF, partial_.as<double>(), dst, ctx_->sms, s);
+    if (ev1) NTF_CUDA(cudaEventRecord(ev1, s));
+  } else {
+    launch_mttkrp_generic(t_->data.p, t_->dtype, v, dF, partial_.as<double>(), segs_[mode], s);
+    if (ev1) NTF_CUDA(cudaEventRecord(ev1, s));
+    launch_reduce_partials(partial_.as<double>(), segs_[mode], v.I * rank_, dst, s);
+  }
+  if (comm.world == 1) return;
+  if (gather) {
+    comm.allgather(gather_.as<double>(), size_t(maxrows_) * rank_, s);
+    const long long* meta = slab_meta_.as<long long>();
+    launch_compact_rows(gather_.as<double>(), maxrows_, meta, meta + comm.world, comm.world, rank_, out, s);
+  } else {
+    comm.allreduce_sum(out, size_t(v.I) * rank_, s);
+  }
+}
+
+// ---- Session -------------------------------------------------------------------
+namespace {
+constexpr int kNnlsScratch = 3072 + 64 * kMaxRank * kMaxRank;
+}
+
+Session::Session(ntf_ctx* ctx, const ntf_tensor* t, int algo, const double* init, int rank,
+                 const ntf_ao_config& cfg, const ntf_her_params* params)
+    : ctx_(ctx), t_(t), algo_(algo), rank_(rank), order_(t->order), cfg_(cfg) {
+  NTF_CUDA(cudaSetDevice(ctx->device));
+  NTF_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+  for (int i = 0; i < order_; ++i) {
+    rows_[i] = int(t->shape[i]);
+    total_factor_len_ += (long long)rows_[i] * rank;
+  }
+  eng_ = std::make_unique<MttkrpEngine>(ctx, t, rank, cfg.flags);
+
+  fac_ = DevBuf(size_t(2 * total_factor_len_) * sizeof(double));
+  if (t->dtype == NTF_DTYPE_F32) fac32_ = DevBuf(size_t(2 * total_factor_len_) * sizeof(float));
+  grams_ = DevBuf(size_t(2 * order_) * rank * rank * sizeof(double));
+  int maxrows = 0;
+  for (int i = 0; i < order_; ++i) maxrows = std::max(maxrows, rows_[i]);
+  C_ = DevBuf(size_t(maxrows) * rank * sizeof(double));
+  state_ = DevBuf(sizeof(RunState));
+  trace_cap_ = cfg.max_outer_iters > 0 ? cfg.max_outer_iters : (1 << 20);
+  trace_ = DevBuf(size_t(trace_cap_) * sizeof(TraceEntry));
+  scratch_ = DevBuf(size_t(kNnlsScratch) * sizeof(double));
+  dF_ = DevBuf(sizeof(DevFactors));
+
+  std::memset(&hF_, 0, sizeof hF_);
+  hF_.order = order_;
+  hF_.rank = rank;
+  long long off = 0;
+  for (int i = 0; i < order_; ++i) {
+    const long long n = (long long)rows_[i] * rank;
+    for (int b = 0; b < 2; ++b) {
+      hF_.x[i][b] = fac_.as<double>() + 2 * off + b * n;
+      if (fac32_.p) hF_.x32[i][b] = fac32_.as<float>() + 2 * off + b * n;
+      hF_.gram[i][b] = grams_.as<double>() + (size_t(2 * i + b)) * rank * rank;
+    }
+    hF_.sel[i] = 0;
+    hF_.rows[i] = rows_[i];
+    NTF_CUDA(cudaMemcpyAsync(hF_.x[i][0], init + off, size_t(n) * sizeof(double), cudaMemcpyHostToDevice, stream_));
+    NTF_CUDA(cudaMemcpyAsync(hF_.x[i][1], init + off, size_t(n) * sizeof(double), cudaMemcpyHostToDevice, stream_));
+    off += n;
+  }
+  NTF_CUDA(cudaMemcpyAsync(dF_.p, &hF_, sizeof hF_, cudaMemcpyHostToDevice, stream_));
+
+  RunState st{};
+  st.beta = params ? params->beta0 : 0.0;
+  st.beta_bar = 1.0;
+  st.nsq = t->nsq;
+  if (params) {
+    st.beta0 = params->beta0;
+    st.gamma = params->gamma;
+    st.gamma_bar = params->gamma_bar;
+    st.eta = params->eta;
+  }
+  st.max_time_s = cfg.max_time_s;
+  st.max_iters = cfg.max_outer_iters > 0 ? cfg.max_outer_iters : trace_cap_;
+  st.inner_max_iters = cfg.inner_stop.max_iters;
+  st.tol = cfg.inner_stop.rel_change_tol;
+  st.algo = algo;
+  NTF_CUDA(cudaMemcpyAsync(state_.p, &st, sizeof st, cudaMemcpyHostToDevice, stream_));
+
+  // GramCache::create + pivot objective f0 (driver_common.hpp:50-56), then
+  // start the run clock (her.cpp:58 / ao.cpp:28).
+  DevFactors* dF = dF_.as<DevFactors>();
+  RunState* dst = state_.as<RunState>();
+  launch_init_factors(dF, hF_, stream_);
+  eng_->run(order_ - 1, dF, C_.as<double>(), stream_);
+  launch_objective(dF, order_, rank, order_ - 1, rows_[order_ - 1], C_.as<double>(), &dst->nsq, &dst->f0,
+                   stream_);
+  NTF_CUDA(cudaMemcpyAsync(&dst->f_prev, &dst->f0, sizeof(double), cudaMemcpyDeviceToDevice, stream_));
+  launch_stamp_start(dst, stream_);
+  NTF_CUDA(cudaHostAlloc(&done_host_, sizeof(int), cudaHostAllocDefault));
+  NTF_CUDA(cudaStreamSynchronize(stream_));
+}
+
+Session::~Session() {
+  if (exec_) cudaGraphExecDestroy(exec_);
+  if (graph_) cudaGraphDestroy(graph_);
+  for (auto e : ev_) cudaEventDestroy(e);
+  if (done_host_) cudaFreeHost(done_host_);
+  if (stream_) {
+    cudaStreamSynchronize(stream_);
+    cudaStreamDestroy(stream_);
+  }
+}
+
+void Session::enqueue_iteration(bool timed) {
+  DevFactors* dF = dF_.as<DevFactors>();
+  RunState* st = state_.as<RunState>();
+  for (int i = 0; i < order_; ++i) {
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (timed) {
+      NTF_CUDA(cudaEventCreate(&e0));
+      NTF_CUDA(cudaEventCreate(&e1));
+      ev_.push_back(e0);
+      ev_.push_back(e1);
+      ev_mode_.push_back(i);
+    }
+    eng_->run(i, dF, C_.as<double>(), stream_, e0, e1);
+    NnlsLaunch a{};
+    a.mode = i;
+    a.order = order_;
+    a.rows = rows_[i];
+    a.rank = rank_;
+    a.role = algo_;
+    a.last = (i == order_ - 1) ? 1 : 0;
+    a.C = C_.as<double>();
+    a.F = dF;
+    a.st = st;
+    a.trace = trace_.as<TraceEntry>();
+    a.scratch = scratch_.as<double>();
+    launch_nnls(a, stream_);
+  }
+}
+
+void Session::build_graph() {
+  if (exec_ || graph_failed_) return;
+  cudaStreamCaptureStatus cs;
+  NTF_CUDA(cudaStreamIsCapturing(stream_, &cs));
+  if (cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+    cudaGetLastError();
+    graph_failed_ = true;
+    return;
+  }
+  bool ok = true;
+  try {
+    enqueue_iteration(false);
+  } catch (...) {
+    ok = false;
+  }
+  cudaGraph_t g = nullptr;
+  if (cudaStreamEndCapture(stream_, &g) != cudaSuccess || !ok) {
+    cudaGetLastError();
+    if (g) cudaGraphDestroy(g);
+    graph_failed_ = true;
+    return;
+  }
+  if (cudaGraphInstantiate(&exec_, g, 0) != cudaSuccess) {
+    cudaGetLastError();
+    cudaGraphDestroy(g);
+    exec_ = nullptr;
+    graph_failed_ = true;
+    return;
+  }
+  graph_ = g;
+}
+
+void Session::step(int iters) {
+  for (int k = 0; k < iters; ++k) {
+    if (timing_) {
+      enqueue_iteration(true);
+    } else if (cfg_.flags & NTF_RUN_NO_GRAPH) {
+      enqueue_iteration(false);
+    } else {
+      if (host_iters_ == 0 && !exec_) {
+        enqueue_iteration(false);  // first iteration direct: sets kernel attributes
+      } else {
+        build_graph();
+        if (exec_)
+          NTF_CUDA(cudaGraphLaunch(exec_, stream_));
+        else
+          enqueue_iteration(false);
+      }
+    }
+    ++host_iters_;
+  }
+}
+
+void Session::sync() { NTF_CUDA(cudaStreamSynchronize(stream_)); }
+
+int Session::iterations() {
+  int k = 0;
+  NTF_CUDA(cudaMemcpyAsync(&k, &state_.as<RunState>()->k, sizeof(int), cudaMemcpyDeviceToHost, stream_));
+  sync();
+  return k;
+}
+
+bool Session::done() {
+  NTF_CUDA(cudaMemcpyAsync(done_host_, &state_.as<RunState>()->done, sizeof(int), cudaMemcpyDeviceToHost, stream_));
+  sync();
+  return *done_host_ != 0;
+}
+
+void Session::factors(double* out) {
+  DevFactors h;
+  NTF_CUDA(cudaMemcpyAsync(&h, dF_.p, sizeof h, cudaMemcpyDeviceToHost, stream_));
+  sync();
+  long long off = 0;
+  for (int i = 0; i < order_; ++i) {
+    const long long n = (long long)rows_[i] * rank_;
+    NTF_CUDA(cudaMemcpyAsync(out + off, h.x[i][h.sel[i]], size_t(n) * sizeof(double), cudaMemcpyDeviceToHost, stream_));
+    off += n;
+  }
+  sync();
+}
+
+void Session::trace(double* f0, ntf_trace_record* out, int cap, int* n) {
+  RunState st;
+  NTF_CUDA(cudaMemcpyAsync(&st, state_.p, sizeof st, cudaMemcpyDeviceToHost, stream_));
+  sync();
+  if (f0) *f0 = st.f0;
+  *n = st.k;
+  const int m = std::min(st.k, cap);
+  if (m <= 0) return;
+  std::vector<TraceEntry> tr(static_cast<size_t>(m));
+  NTF_CUDA(cudaMemcpyAsync(tr.data(), trace_.p, size_t(m) * sizeof(TraceEntry), cudaMemcpyDeviceToHost, stream_));
+  sync();
+  for (int i = 0; i < m; ++i) {
+    ntf_trace_record r{};
+    r.iter = i + 1;
+    r.time_s = tr[size_t(i)].time_s;
+    r.f = tr[size_t(i)].f;
+    if (algo_ == 0) {
+      r.has_restarted = 1;
+      r.restarted = tr[size_t(i)].restarted;
+      r.has_beta = 1;
+      r.beta = tr[size_t(i)].beta;
+    }
+    out[i] = r;
+  }
+}
+
+void Session::set_kernel_timing(bool on) { timing_ = on; }
+
+void Session::kernel_times(double* ms_per_mode, int* launches, int* total_kernels) {
+  sync();
+  for (size_t k = 0; k < ev_mode_.size(); ++k) {
+    float ms = 0.f;
+    NTF_CUDA(cudaEventElapsedTime(&ms, ev_[2 * k], ev_[2 * k + 1]));
+    kernel_ms_[ev_mode_[k]] += ms;
+    kernel_n_[ev_mode_[k]] += 1;
+  }
+  for (auto e : ev_) cudaEventDestroy(e);
+  ev_.clear();
+  ev_mode_.clear();
+  int total = 0;
+  for (int i = 0; i < order_; ++i) {
+    if (ms_per_mode) ms_per_mode[i] = kernel_ms_[i];
+    if (launches) launches[i] = kernel_n_[i];
+    total += eng_->kernels_per_call(i) + 1;  // MTTKRP kernels + fused NNLS
+  }
+  if (total_kernels) *total_kernels = total;
+}
+
+}  // namespace ntfb
+
+ntf_ctx::~ntf_ctx() {
+  if (stream) cudaStreamDestroy(stream);
+}

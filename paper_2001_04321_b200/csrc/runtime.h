@@ -1,0 +1,142 @@
+// Host runtime of libntf_b200.so: contexts, device tensors, the MTTKRP
+// engine (kernel choice + deterministic reduction + NCCL exchange) and the
+// GPU-resident HER / AO sessions behind ntf_her_run / ntf_ao_run.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <memory>
+#include <vector>
+
+#include "ntf_internal.h"
+
+struct ntf_ctx;
+struct ntf_tensor;
+
+namespace ntfb {
+
+// ---- datagen / metrics (datagen.cpp) ---------------------------------------
+uint64_t stream_seed(uint64_t base, uint64_t stream);
+void random_init(const int* shape, int order, int rank, uint64_t seed, double* out);
+void generate(const int* shape, int order, int rank, double sigma, int ill, int collinear, uint64_t seed,
+              int dtype, void* tensor, double* truth);
+double factor_error(const double* est, const double* truth, const int* shape, int order, int rank);
+
+// ---- device memory ------------------------------------------------------------
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  DevBuf() = default;
+  explicit DevBuf(size_t n);
+  ~DevBuf();
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), bytes(o.bytes) { o.p = nullptr; o.bytes = 0; }
+  DevBuf& operator=(DevBuf&& o) noexcept;
+  template <typename T>
+  T* as() const { return static_cast<T*>(p); }
+};
+
+// ---- collectives ---------------------------------------------------------------
+struct Comm {
+  void* nccl = nullptr;  // ncclComm_t
+  int rank = 0, world = 1;
+  void allreduce_sum(double* buf, size_t n, cudaStream_t s) const;
+  void allgather(double* buf, size_t n_per_rank, cudaStream_t s) const;  // in place
+  ~Comm();
+};
+
+void slab_range(long long dim0, int rank, int world, long long* begin, long long* end);
+
+// ---- MTTKRP engine -------------------------------------------------------------
+// Owns the split-K partial workspace; produces the FULL I_mode x r FP64
+// MTTKRP (identical on every rank) in `out`.
+class MttkrpEngine {
+ public:
+  MttkrpEngine(const ntf_ctx* ctx, const ntf_tensor* t, int rank, unsigned flags);
+  // Enqueue on `s`. With kernel timing on, the main kernel of each call is
+  // bracketed by events ev[0], ev[1] (may be null).
+  void run(int mode, const DevFactors* dF, double* out, cudaStream_t s, cudaEvent_t ev0 = nullptr,
+           cudaEvent_t ev1 = nullptr);
+  int kernels_per_call(int mode) const;
+  ModeView view(int mode) const;
+
+ private:
+  const ntf_ctx* ctx_;
+  const ntf_tensor* t_;
+  int rank_;
+  unsigned flags_;
+  int segs_[kMaxOrder];
+  DevBuf partial_;
+  DevBuf gather_;                // padded rows for the mode-1 allgather
+  DevBuf slab_meta_;             // begins/counts (long long) per rank
+  long long maxrows_ = 0;
+};
+
+// ---- GPU-resident solver session ---------------------------------------------
+class Session {
+ public:
+  Session(ntf_ctx* ctx, const ntf_tensor* t, int algo, const double* init, int rank, const ntf_ao_config& cfg,
+          const ntf_her_params* params);
+  ~Session();
+  void step(int iters);
+  void sync();
+  int iterations();
+  bool done();
+  void factors(double* out);
+  void trace(double* f0, ntf_trace_record* out, int cap, int* n);
+  void set_kernel_timing(bool on);
+  void kernel_times(double* ms_per_mode, int* launches, int* total_kernels);
+  cudaStream_t stream() const { return stream_; }
+  int order() const { return order_; }
+
+ private:
+  void enqueue_iteration(bool timed);
+  void build_graph();
+
+  ntf_ctx* ctx_;
+  const ntf_tensor* t_;
+  int algo_, rank_, order_;
+  int rows_[kMaxOrder];
+  long long total_factor_len_ = 0;
+  ntf_ao_config cfg_;
+  cudaStream_t stream_ = nullptr;
+  std::unique_ptr<MttkrpEngine> eng_;
+  DevFactors hF_{};
+  DevBuf dF_, fac_, fac32_, grams_, C_, state_, trace_, scratch_, counter_;
+  int trace_cap_ = 0;
+  cudaGraph_t graph_ = nullptr;
+  cudaGraphExec_t exec_ = nullptr;
+  bool graph_failed_ = false;
+  bool timing_ = false;
+  std::vector<cudaEvent_t> ev_;
+  std::vector<int> ev_mode_;
+  double kernel_ms_[kMaxOrder] = {};
+  int kernel_n_[kMaxOrder] = {};
+  int host_iters_ = 0;  // iterations enqueued
+  int* done_host_ = nullptr;  // pinned mirror
+};
+
+}  // namespace ntfb
+
+// Opaque ABI objects.
+struct ntf_ctx {
+  int device = 0;
+  int sms = 0;
+  cudaStream_t stream = nullptr;
+  ntfb::Comm comm;
+  ntfb::DevBuf scratch;  // small shared scratch (norms, standalone NNLS)
+  ~ntf_ctx();
+};
+
+struct ntf_tensor {
+  ntf_ctx* ctx = nullptr;
+  int dtype = NTF_DTYPE_F64;
+  int order = 0;
+  long long shape[NTF_MAX_ORDER] = {};  // full shape
+  long long row0 = 0, rows = 0;         // local mode-1 slab
+  long long n_local = 0;
+  ntfb::DevBuf data;
+  ntfb::DevBuf nsq_dev;  // ||T||^2 (global, FP64) on the device
+  double nsq = 0.0;
+};

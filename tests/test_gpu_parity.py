@@ -1,0 +1,268 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the CPU oracle.
+
+Mirrors the reference's hot-path pins: MTTKRP vs unfold*KR
+on random shapes (test_kernels.cpp:138-153), rank-one identity (:121-136),
+objective vs residual (:222-248), AHALS (test_nnls.cpp:56-112), HER/AO traces
+(test_her.cpp, test_ao.cpp), plus whole-trace parity with the oracle.
+"""
+import numpy as np
+import pytest
+
+from parity import compare_traces, rel_fro
+
+pytestmark = pytest.mark.gpu
+
+
+def _shape_gen(gen, max_order=4):
+    order = 2 + int(gen.integers(0, max_order - 1))
+    return [int(gen.integers(1, 7)) for _ in range(order)]
+
+
+# ---- MTTKRP -----------------------------------------------------------------------
+
+def test_mttkrp_rank_one_identity_and_zero(P, oracle):
+    gen = np.random.default_rng(6)
+    m = [gen.random((d, 1)) for d in (3, 4, 2)]
+    t = oracle.reconstruct(m)
+    prov = P.GpuDenseProvider(t)
+    want = m[0] * (np.sum(m[1] ** 2) * np.sum(m[2] ** 2))
+    assert rel_fro(prov.mttkrp(m, 0), want) < 1e-14
+    z = P.GpuDenseProvider(np.zeros((3, 4, 2)))
+    assert np.abs(z.mttkrp(m, 1)).max() == 0.0
+    with pytest.raises(ValueError):
+        prov.mttkrp([gen.random((d, 1)) for d in (3, 4, 3)], 0)
+
+
+def test_mttkrp_random_shapes_vs_enumeration(P, oracle):
+    gen = np.random.default_rng(7)
+    for _ in range(40):
+        shape = _shape_gen(gen)
+        r = 1 + int(gen.integers(0, 4))
+        t = gen.uniform(-1, 1, shape)
+        m = [gen.uniform(-1, 1, (d, r)) for d in shape]
+        prov = P.GpuDenseProvider(t)
+        for mode in range(len(shape)):
+            assert rel_fro(prov.mttkrp(m, mode), oracle.ref_mttkrp(t, m, mode)) < 1e-12
+
+
+@pytest.mark.parametrize("shape,rank", [([50, 50, 50], 10), ([37, 41, 29], 20), ([20, 21, 22, 23], 16),
+                                        ([300, 30, 30], 20), ([8, 200, 64], 12), ([64, 48, 32], 32),
+                                        ([40, 30, 20], 64)])
+def test_mttkrp_medium_f64(P, oracle, shape, rank):
+    gen = np.random.default_rng(sum(shape) + rank)
+    t = gen.random(shape)
+    m = [gen.random((d, rank)) for d in shape]
+    prov = P.GpuDenseProvider(t)
+    for mode in range(len(shape)):
+        assert rel_fro(prov.mttkrp(m, mode), oracle.mttkrp(t, m, mode)) < 1e-12
+
+
+@pytest.mark.parametrize("shape,rank", [([50, 50, 50], 10), ([60, 50, 40], 32), ([30, 20, 40], 64)])
+def test_mttkrp_f32(P, oracle, shape, rank):
+    gen = np.random.default_rng(3 + rank)
+    t = gen.random(shape).astype(np.float32)
+    m = [gen.random((d, rank)) for d in shape]
+    prov = P.GpuDenseProvider(t)
+    for mode in range(len(shape)):
+        assert rel_fro(prov.mttkrp(m, mode), oracle.mttkrp(t, m, mode)) < 1e-5
+
+
+def test_objective_vs_residual(P, oracle):
+    gen = np.random.default_rng(10)
+    m = [gen.random((d, 2)) for d in (3, 4, 2)]
+    t = oracle.reconstruct(m)
+    prov = P.GpuDenseProvider(t)
+    nsq = prov.norm_sq()
+    assert abs(prov.objective(m)) <= 1e-12 * nsq
+    z = [np.zeros((d, 2)) for d in (3, 4, 2)]
+    assert abs(prov.objective(z) - 0.5 * nsq) <= 1e-14 * nsq
+    for _ in range(30):
+        shape = _shape_gen(gen)
+        r = 1 + int(gen.integers(0, 4))
+        rt = gen.random(shape)
+        rm = [gen.random((d, r)) for d in shape]
+        want = oracle.ref_objective(rt, rm)
+        p = P.GpuDenseProvider(rt)
+        for pivot in range(len(shape)):
+            assert abs(p.objective(rm, pivot) - want) <= 1e-10 * abs(want)
+
+
+def test_norm_sq(P, oracle):
+    gen = np.random.default_rng(1)
+    t = gen.random((37, 23, 19))
+    assert abs(P.GpuDenseProvider(t).norm_sq() - oracle.norm_sq(t)) <= 1e-13 * oracle.norm_sq(t)
+
+
+# ---- AHALS --------------------------------------------------------------------------
+
+def _convex_problem(gen, rows, r):
+    rm = gen.uniform(-1, 1, (r + 2, r))
+    g = rm.T @ rm + 0.1 * np.eye(r)
+    return g, gen.uniform(-1, 1, (rows, r)), gen.random((rows, r))
+
+
+def test_ahals_basic_properties(P, oracle):
+    gen = np.random.default_rng(1)
+    c = gen.uniform(-1, 1, (5, 3))
+    out = P.solve_nnls(P.NnlsSolver.ahals, np.eye(3), c, np.zeros((5, 3)), P.InnerStop(1, 1e-2))
+    assert np.array_equal(out, np.maximum(c, 0.0))
+    neg = -gen.random((5, 3))
+    assert np.abs(P.solve_nnls(0, np.eye(3), neg, np.zeros((5, 3)), P.InnerStop(1, 1e-2))).max() == 0.0
+    # degenerate column untouched
+    g = np.zeros((2, 2))
+    g[0, 0] = 1.0
+    w0 = gen.random((3, 2))
+    out = P.solve_nnls(0, g, gen.uniform(-1, 1, (3, 2)), w0, P.InnerStop(1, 1e-2))
+    assert np.array_equal(out[:, 1], w0[:, 1])
+    # fixed point stops early
+    c = gen.uniform(-1, 1, (4, 3))
+    assert np.array_equal(P.solve_nnls(0, np.eye(3), c, np.maximum(c, 0), P.InnerStop(50, 1e-2)), np.maximum(c, 0))
+    with pytest.raises(P.UnsupportedError):
+        P.solve_nnls(P.NnlsSolver.admm, np.eye(3), c, np.maximum(c, 0))
+
+
+@pytest.mark.parametrize("rows,r", [(4, 2), (6, 3), (300, 20), (500, 32), (100, 16), (2000, 64), (1100, 10)])
+def test_ahals_vs_oracle(P, oracle, rows, r):
+    gen = np.random.default_rng(rows * 7 + r)
+    g, c, w0 = _convex_problem(gen, rows, r)
+    c = c * 10
+    for it in (1, 5, 50):
+        got, sw = P.solve_nnls(0, g, c, w0, P.InnerStop(it, 1e-2), return_sweeps=True)
+        want, sw_o = oracle.ahals_solve(g, c, w0, it, 1e-2, return_sweeps=True)
+        assert sw == sw_o
+        assert rel_fro(got, want) < 1e-12
+
+
+# ---- drivers -------------------------------------------------------------------------
+
+def _instance(P, shape, rank, sigma, seed, ill=False):
+    spec = P.SyntheticSpec(shape=shape, rank=rank, noise_sigma=sigma, ill_conditioned=ill, seed=seed)
+    t, truth = P.generate(spec)
+    init = P.random_init(shape, rank, P.stream_seed(seed, 1))
+    return t, truth, init
+
+
+@pytest.mark.parametrize("shape,rank,sigma,seed", [([50, 50, 50], 10, 0.01, 101), ([30, 30, 30], 5, 0.0, 4000),
+                                                   ([8, 7, 6], 3, 0.05, 7), ([20, 20, 20, 20], 4, 0.01, 103),
+                                                   ([12, 9], 2, 0.01, 402), ([15, 12, 10], 4, 0.001, 97)])
+def test_her_trace_parity(P, oracle, shape, rank, sigma, seed):
+    t, truth, init = _instance(P, shape, rank, sigma, seed, ill=(seed == 97))
+    cfg = P.AoConfig(max_outer_iters=50)
+    model, trace = P.her_run(t, init, cfg, P.HerParams())
+    fo, f0, recs = oracle.run("her", t, init.factors, max_outer_iters=50)
+    stats = compare_traces(trace, f0, recs, oracle.norm_sq(t))
+    assert stats["checked"] == 50
+    trace.validate()
+    assert model.is_nonnegative()
+
+
+@pytest.mark.parametrize("shape,rank,sigma,seed", [([50, 50, 50], 10, 0.01, 101), ([6, 5, 4], 3, 0.1, 29),
+                                                   ([5, 4, 3, 6], 2, 0.01, 404)])
+def test_ao_trace_parity(P, oracle, shape, rank, sigma, seed):
+    t, truth, init = _instance(P, shape, rank, sigma, seed)
+    cfg = P.AoConfig(max_outer_iters=50)
+    model, trace = P.ao_run(t, init, cfg)
+    fo, f0, recs = oracle.run("ao", t, init.factors, max_outer_iters=50)
+    compare_traces(trace, f0, recs, oracle.norm_sq(t), check_restarts=False)
+    prev = trace.f0
+    for r in trace.records:  # monotone (test_ao.cpp:83-104)
+        assert r.f <= prev + 1e-12 * trace.f0
+        prev = r.f
+    for a, b in zip(model, fo):
+        assert rel_fro(a, b) < 1e-6
+
+
+def test_beta_zero_reduces_to_ao(P):
+    """test_her.cpp:113-135 / acceptance.cpp:387-415 on the GPU path."""
+    for seed in (101, 102, 103, 104, 105):
+        t, _, _ = _instance(P, [6, 5, 4], 2, 0.05, seed)
+        init = P.random_init([6, 5, 4], 2, seed + 1000)
+        cfg = P.AoConfig(max_outer_iters=50)
+        _, at = P.ao_run(t, init, cfg)
+        _, ht = P.her_run(t, init, cfg, P.HerParams(beta0=1e-300))
+        assert len(at.records) == len(ht.records) == 50
+        for a, h in zip(at.records, ht.records):
+            assert abs(h.f - a.f) <= 1e-12 * max(abs(a.f), abs(h.f))
+
+
+def test_her_bookkeeping_observer(P):
+    """test_her.cpp:137-179."""
+    t, _, _ = _instance(P, [8, 7, 6], 3, 0.05, 7)
+    init = P.random_init([8, 7, 6], 3, 71)
+    seen = []
+
+    def obs(info):
+        assert info.factors.is_nonnegative() and info.hat_factors.is_nonnegative()
+        if info.restarted:
+            for a, h in zip(info.factors, info.hat_factors):
+                assert np.array_equal(a, h)
+        seen.append(info.restarted)
+
+    model, trace = P.her_run(t, init, P.AoConfig(max_outer_iters=200), P.HerParams(), observer=obs)
+    trace.validate()
+    assert len(seen) == 200 and trace.restart_count() == sum(seen)
+    prev = trace.f0
+    for r in trace.records:
+        if not r.restarted:
+            assert r.f <= prev + 1e-12 * trace.f0
+            prev = r.f
+
+
+def test_her_beats_ao_noiseless(P):
+    """test_her.cpp:181-204."""
+    her_f, ao_f = [], []
+    for s in range(5):
+        t, _, _ = _instance(P, [15, 15, 15], 3, 0.0, 200 + s)
+        init = P.random_init([15, 15, 15], 3, 300 + s)
+        cfg = P.AoConfig(max_outer_iters=150)
+        ao_f.append(P.ao_run(t, init, cfg)[1].final_f())
+        her_f.append(P.her_run(t, init, cfg, P.HerParams())[1].final_f())
+    assert sorted(her_f)[2] < sorted(ao_f)[2]
+
+
+def test_identical_inputs_identical_traces(P):
+    t, _, _ = _instance(P, [6, 6, 6], 2, 0.01, 83)
+    init = P.random_init([6, 6, 6], 2, 89)
+    cfg = P.AoConfig(max_outer_iters=40)
+    _, a = P.her_run(t, init, cfg)
+    _, b = P.her_run(t, init, cfg)
+    assert [(r.f, r.beta, r.restarted) for r in a.records] == [(r.f, r.beta, r.restarted) for r in b.records]
+
+
+def test_time_budget_and_factor_error(P):
+    t, truth, _ = _instance(P, [10, 10, 10], 3, 0.0, 47)
+    cfg = P.AoConfig(max_time_s=0.05)
+    _, trace = P.ao_run(t, P.random_init([10, 10, 10], 3, 51), cfg)
+    assert trace.records and trace.records[-1].time_s >= 0.05
+    t, truth, _ = _instance(P, [6, 6, 6], 2, 0.0, 53)
+    cfg = P.AoConfig(max_outer_iters=30, record_factor_error=True, ground_truth=truth)
+    _, trace = P.ao_run(t, P.random_init([6, 6, 6], 2, 57), cfg)
+    assert trace.records[-1].e is not None and trace.records[-1].e < trace.records[0].e
+
+
+def test_rank_one_fit_and_exact_factorization(P, oracle):
+    """test_ao.cpp:35-54."""
+    t, _, _ = _instance(P, [2, 2, 2], 1, 0.0, 3)
+    _, trace = P.ao_run(t, P.random_init([2, 2, 2], 1, 17), P.AoConfig(max_outer_iters=50))
+    nsq = oracle.norm_sq(t)
+    assert trace.final_f() <= 1e-12 * nsq and len(trace.records) == 50
+    gen = np.random.default_rng(5)
+    exact = [gen.uniform(0.1, 1.0, (d, 2)) for d in (4, 3, 3)]
+    t = oracle.reconstruct(exact)
+    _, trace = P.ao_run(t, exact, P.AoConfig(max_outer_iters=10))
+    for r in trace.records:
+        assert abs(r.f) <= 1e-12 * oracle.norm_sq(t)
+
+
+def test_driver_validation(P):
+    t, _, init = _instance(P, [5, 5, 5], 2, 0.0, 1)
+    with pytest.raises(ValueError):
+        P.her_run(t, init, P.AoConfig())  # no budget
+    with pytest.raises(ValueError):
+        P.her_run(t, init, P.AoConfig(max_outer_iters=3), P.HerParams(beta0=0.0))
+    bad = [f.copy() for f in init]
+    bad[0][0, 0] = -1.0
+    with pytest.raises(ValueError):
+        P.her_run(t, bad, P.AoConfig(max_outer_iters=3))
+    with pytest.raises(P.UnsupportedError):
+        P.her_run(t, init, P.AoConfig(solver=P.NnlsSolver.admm, max_outer_iters=3))

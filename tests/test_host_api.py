@@ -1,0 +1,136 @@
+"""Host-side checks of the product library that need no GPU: the C ABI loads
+and exports every symbol include/ntf_b200.h declares, host datagen is
+bit-exact with the oracle (and hence the reference generator), validation
+mirrors the reference's exceptions, trace CSV round-trips, and there is no
+CPU fallback (a context cannot be created without a device)."""
+import ctypes as C
+import os
+import re
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_library_exports_every_declared_symbol(P):
+    from paper_2001_04321_b200 import _lib
+    header = open(os.path.join(ROOT, "include", "ntf_b200.h")).read()
+    declared = sorted(set(re.findall(r"^\s*(?:[A-Za-z_][\w ]*\*?\s*\**)\b(ntf_\w+)\s*\(", header, re.M)))
+    assert len(declared) >= 30
+    lib = C.CDLL(_lib.LIB_PATH)
+    missing = [name for name in declared if not hasattr(lib, name)]
+    assert not missing, missing
+    assert set(declared) == set(_lib.SIGNATURES), set(declared) ^ set(_lib.SIGNATURES)
+
+
+@pytest.mark.parametrize("shape,rank,sigma,ill,seed", [([6, 5, 4], 3, 0.1, False, 42), ([30, 20, 10], 5, 0.01, True, 7),
+                                                      ([5, 4, 3, 6], 2, 0.01, False, 404), ([12, 9], 2, 0.0, False, 1),
+                                                      ([50, 50, 50], 10, 0.01, False, 101), ([7], 2, 0.5, False, 3)])
+def test_generate_bit_exact_with_oracle(P, oracle, shape, rank, sigma, ill, seed):
+    t, truth = P.generate(P.SyntheticSpec(shape, rank, sigma, ill, seed))
+    t2, truth2 = oracle.generate(shape, rank, sigma, ill, seed)
+    assert np.array_equal(t, t2)
+    for a, b in zip(truth, truth2):
+        assert np.array_equal(a, b)
+    t32, _ = P.generate(P.SyntheticSpec(shape, rank, sigma, ill, seed), dtype=np.float32)
+    assert t32.dtype == np.float32 and np.array_equal(t32, t2.astype(np.float32))
+
+
+def test_collinear_rule_matches_oracle(P, oracle):
+    spec = P.SyntheticSpec([9, 8, 7], 4, 0.01, False, 104, collinear=True)
+    t, truth = P.generate(spec)
+    t2, truth2 = oracle.generate([9, 8, 7], 4, 0.01, False, 104, collinear=True)
+    assert np.array_equal(t, t2)
+    # columns share one vector: pairwise column differences are 0.5 (U_j - U_k)
+    _, plain = oracle.generate([9, 8, 7], 4, 0.0, False, 104)
+    for a, u in zip(truth, plain):
+        assert np.allclose(a[:, 0] - a[:, 1], 0.5 * (u[:, 0] - u[:, 1]), atol=1e-15)
+
+
+def test_random_init_and_stream_seed(P, oracle):
+    for seed in (0, 17, 2**40 + 3):
+        a = P.random_init([4, 6, 3], 3, seed)
+        b = oracle.random_init([4, 6, 3], 3, seed)
+        assert all(np.array_equal(x, y) for x, y in zip(a, b))
+        assert P.stream_seed(seed, 3) == oracle.stream_seed(seed, 3)
+
+
+def test_factor_error_matches_oracle(P, oracle):
+    gen = np.random.default_rng(4)
+    truth = [gen.random((d, 4)) for d in (5, 6, 7)]
+    est = [a + 0.05 * gen.random(a.shape) for a in truth]
+    assert P.factor_error(est, truth) == pytest.approx(oracle.factor_error(est, truth), rel=1e-12)
+    perm = [2, 0, 3, 1]
+    assert P.factor_error([a[:, perm] * 3.0 for a in truth], truth) < 1e-12
+
+
+def test_validation_mirrors_reference(P):
+    with pytest.raises(ValueError):
+        P.HerParams(beta0=0.0).validate()
+    with pytest.raises(ValueError):
+        P.HerParams(gamma_bar=1.0).validate()
+    with pytest.raises(ValueError):
+        P.HerParams(eta=1.01).validate()
+    P.HerParams().validate()
+    with pytest.raises(ValueError):
+        P.AoConfig().validate()
+    with pytest.raises(ValueError):
+        P.AoConfig(max_outer_iters=5, record_factor_error=True).validate()
+    P.AoConfig(max_outer_iters=5).validate()
+    with pytest.raises(ValueError):
+        P.generate(P.SyntheticSpec([3, 3], 0))
+    with pytest.raises(ValueError):
+        P.generate(P.SyntheticSpec([3, 3], 1, ill_conditioned=True))
+    with pytest.raises(ValueError):
+        P.generate(P.SyntheticSpec([3, 3], 1, noise_sigma=-0.5))
+    assert P.nnls_solver_from_name("as") == P.NnlsSolver.active_set
+    with pytest.raises(ValueError):
+        P.nnls_solver_from_name("lbfgs")
+
+
+def test_update_betas_host_mirror(P, oracle):
+    gen = np.random.default_rng(2)
+    s = P.HerState(beta=0.5, beta_bar=1.0)
+    b, bb = 0.5, 1.0
+    for _ in range(1000):
+        rs = bool(gen.integers(0, 2))
+        P.update_betas(s, rs, P.HerParams())
+        b, bb = oracle.update_betas(b, bb, rs)
+        assert (s.beta, s.beta_bar) == (b, bb)
+
+
+def test_slab_range_partitions_mode1(P):
+    for dim0 in (1, 7, 100, 300, 2000):
+        for world in (1, 2, 3, 4, 8):
+            if world > dim0:
+                continue
+            spans = [P.slab_range(dim0, r, world) for r in range(world)]
+            assert spans[0][0] == 0 and spans[-1][1] == dim0
+            assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
+            sizes = [e - b for b, e in spans]
+            assert max(sizes) - min(sizes) <= 1
+    with pytest.raises(ValueError):
+        P.slab_range(10, 2, 2)
+
+
+def test_trace_csv_round_trip(P, tmp_path):
+    tr = P.RunTrace(1.5, [P.TraceRecord(1, 0.1, 1.25, None, False, 0.5),
+                          P.TraceRecord(2, 0.2, 1.0 / 3.0, 0.25, True, 0.525)])
+    path = tmp_path / "t.csv"
+    tr.write_csv(str(path))
+    assert open(path).readline().strip() == "iter,time_s,f,e,restarted,beta"
+    back = P.RunTrace.read_csv(str(path))
+    assert [(r.iter, r.f, r.e, r.restarted, r.beta) for r in back.records] == \
+        [(r.iter, r.f, r.e, r.restarted, r.beta) for r in tr.records]
+    back.validate()
+    assert back.restart_count() == 1 and back.final_f() == 1.0 / 3.0
+
+
+def test_no_cpu_fallback_without_device(P):
+    if P.device_count() > 0:
+        pytest.skip("a GPU is present")
+    with pytest.raises(P.CudaError):
+        P.Context(0)
+    with pytest.raises(P.CudaError):
+        P.GpuDenseProvider(np.ones((2, 2, 2)))
