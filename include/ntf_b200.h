@@ -93,7 +93,7 @@ typedef struct {
   int has_restarted;
   int restarted;
   int has_beta;
-  int reserved;
+  int inner_sweeps; /* AHALS passes summed over the modes of the iteration */
   double time_s;
   double f;
   double e;
@@ -176,6 +176,10 @@ int ntf_mttkrp(ntf_ctx* ctx, const ntf_tensor* t, const double* factors, int ran
  * (-1 = last mode) plus the cheap objective. */
 int ntf_objective(ntf_ctx* ctx, const ntf_tensor* t, const double* factors, int rank, int pivot,
                   double* out);
+
+/* Diagnostics: the kernel plan ntf_mttkrp uses for (rank, mode) on this
+ * tensor ("generic" or the fast-path blocking), NUL-terminated into buf. */
+int ntf_mttkrp_plan(ntf_ctx* ctx, const ntf_tensor* t, int rank, int mode, char* buf, size_t n);
 
 /* ---- inner solver (include/ntf/nnls.hpp:12-55) --------------------------- */
 /* solve_nnls(solver, {gram, target, init}, stop) on the GPU. gram: r x r,

@@ -48,7 +48,7 @@ class HerParamsC(C.Structure):
 
 class TraceRecordC(C.Structure):
     _fields_ = [("iter", C.c_int), ("has_e", C.c_int), ("has_restarted", C.c_int), ("restarted", C.c_int),
-                ("has_beta", C.c_int), ("reserved", C.c_int), ("time_s", C.c_double), ("f", C.c_double),
+                ("has_beta", C.c_int), ("inner_sweeps", C.c_int), ("time_s", C.c_double), ("f", C.c_double),
                 ("e", C.c_double), ("beta", C.c_double)]
 
 
@@ -86,6 +86,7 @@ SIGNATURES = {
     "ntf_tensor_norm_sq": (C.c_int, [C.c_void_p, dptr]),
     "ntf_tensor_destroy": (C.c_int, [C.c_void_p]),
     "ntf_mttkrp": (C.c_int, [C.c_void_p, C.c_void_p, dptr, C.c_int, C.c_int, dptr]),
+    "ntf_mttkrp_plan": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_char_p, C.c_size_t]),
     "ntf_objective": (C.c_int, [C.c_void_p, C.c_void_p, dptr, C.c_int, C.c_int, dptr]),
     "ntf_solve_nnls": (C.c_int, [C.c_void_p, C.c_int, dptr, dptr, dptr, C.c_int, C.c_int,
                                  C.POINTER(InnerStopC), dptr, iptr]),

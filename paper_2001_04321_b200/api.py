@@ -207,6 +207,7 @@ class TraceRecord:
     e: Optional[float] = None
     restarted: Optional[bool] = None
     beta: Optional[float] = None
+    inner_sweeps: Optional[int] = None  # diagnostics: AHALS passes summed over modes
 
 
 @dataclasses.dataclass
@@ -442,6 +443,12 @@ class GpuDenseProvider(ObjectiveProvider):
         _check(L.lib().ntf_mttkrp(self.ctx.handle, self.handle, _dp(flat), m.rank(), mode, _dp(out)))
         return out
 
+    def mttkrp_plan(self, rank, mode):
+        """Which kernel ntf_mttkrp runs for (rank, mode): 'generic' or the fast blocking."""
+        buf = C.create_string_buffer(512)
+        _check(L.lib().ntf_mttkrp_plan(self.ctx.handle, self.handle, rank, mode, buf, len(buf)))
+        return buf.value.decode()
+
     def objective(self, model, pivot=-1):
         """kernels.cpp:305-311 (one MTTKRP + the cheap objective)."""
         m, flat = self._model_flat(model)
@@ -515,7 +522,7 @@ def _records(buf, n, cap):
         r = buf[i]
         out.append(TraceRecord(r.iter, r.time_s, r.f, r.e if r.has_e else None,
                                bool(r.restarted) if r.has_restarted else None,
-                               r.beta if r.has_beta else None))
+                               r.beta if r.has_beta else None, r.inner_sweeps))
     return out
 
 

@@ -459,6 +459,21 @@ int ntf_mttkrp(ntf_ctx* ctx, const ntf_tensor* t, const double* factors, int ran
   });
 }
 
+int ntf_mttkrp_plan(ntf_ctx* ctx, const ntf_tensor* t, int rank, int mode, char* buf, size_t n) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(t, "tensor");
+    need(buf, "buf");
+    if (mode < 0 || mode >= t->order) throw InvalidArgument("mode out of range");
+    MttkrpEngine eng(ctx, t, rank, 0);
+    const std::string s = eng.describe(mode);
+    if (n) {
+      std::strncpy(buf, s.c_str(), n - 1);
+      buf[n - 1] = '\0';
+    }
+  });
+}
+
 int ntf_objective(ntf_ctx* ctx, const ntf_tensor* t, const double* factors, int rank, int pivot, double* out) {
   return guarded([&] {
     need(ctx, "ctx");

@@ -95,14 +95,30 @@ __global__ void __launch_bounds__(kGenThreads)
     partial[(seg * v.I + mid) * r + c0 + threadIdx.x] = sm[threadIdx.x * kGenThreads];
 }
 
-__global__ void reduce_partials_kernel(const double* __restrict__ partial, int segs, long long n,
-                                       double* __restrict__ out) {
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
-       i += (long long)gridDim.x * blockDim.x) {
-    double s = 0.0;
-    for (int k = 0; k < segs; ++k) s += partial[k * n + i];
-    out[i] = s;
+// out[i] = sum_k partial[k][i]. A block covers 64 outputs with 4 slot
+// groups (k mod 4) of 64 threads; each thread keeps 4 interleaved sums so
+// 4 independent loads are in flight, and the groups are folded in a fixed
+// order: the result depends only on `segs`, never on scheduling.
+constexpr int kRedOut = 64;
+__global__ void __launch_bounds__(256) reduce_partials_kernel(const double* __restrict__ partial, int segs,
+                                                              long long n, double* __restrict__ out) {
+  __shared__ double sm[4][kRedOut];
+  const int e = threadIdx.x % kRedOut, g = threadIdx.x / kRedOut;
+  const long long i = blockIdx.x * (long long)kRedOut + e;
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  if (i < n) {
+    int k = g;
+    for (; k + 12 < segs; k += 16) {
+      a0 += __ldg(&partial[(long long)k * n + i]);
+      a1 += __ldg(&partial[(long long)(k + 4) * n + i]);
+      a2 += __ldg(&partial[(long long)(k + 8) * n + i]);
+      a3 += __ldg(&partial[(long long)(k + 12) * n + i]);
+    }
+    for (; k < segs; k += 4) a0 += __ldg(&partial[(long long)k * n + i]);
   }
+  sm[g][e] = (a0 + a1) + (a2 + a3);
+  __syncthreads();
+  if (g == 0 && i < n) out[i] = (sm[0][e] + sm[1][e]) + (sm[2][e] + sm[3][e]);
 }
 
 constexpr int kNormBlocks = 592;  // fixed, so the sum order is device-independent
@@ -222,9 +238,8 @@ void launch_mttkrp_generic(const void* t, int dtype, const ModeView& v, const De
 }
 
 void launch_reduce_partials(const double* partial, int segs, long long n, double* out, cudaStream_t s) {
-  const int threads = 256;
-  const long long blocks = std::min<long long>((n + threads - 1) / threads, 4096);
-  reduce_partials_kernel<<<unsigned(blocks), threads, 0, s>>>(partial, segs, n, out);
+  const long long blocks = (n + kRedOut - 1) / kRedOut;
+  reduce_partials_kernel<<<unsigned(blocks), 256, 0, s>>>(partial, segs, n, out);
   NTF_CUDA(cudaGetLastError());
 }
 

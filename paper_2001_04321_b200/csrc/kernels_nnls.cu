@@ -41,8 +41,10 @@ __device__ double block_sum(double v, double* red) {
   if (lane == 0) red[warp] = v;
   __syncthreads();
   double s = 0.0;
+  const int nw = blockDim.x >> 5;
 #pragma unroll
-  for (int w = 0; w < TPB / 32; ++w) s += red[w];
+  for (int w = 0; w < TPB / 32; ++w)
+    if (w < nw) s += red[w];
   return s;
 }
 
@@ -69,11 +71,12 @@ template <int RP, int TPB>
 __device__ void cta_gram(const double* stage, int r, double* dst, double* slots, cg::grid_group& grid) {
   constexpr int LD = RP + 1;
   const bool multi = gridDim.x > 1;
-  for (int e = threadIdx.x; e < r * r; e += TPB) {
+  const int nt = blockDim.x;
+  for (int e = threadIdx.x; e < r * r; e += nt) {
     const int p = e / r, q = e % r;
     if (p > q) continue;
     double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-    for (int i = 0; i < TPB; i += 4) {
+    for (int i = 0; i < nt; i += 4) {
       s0 += stage[(i + 0) * LD + p] * stage[(i + 0) * LD + q];
       s1 += stage[(i + 1) * LD + p] * stage[(i + 1) * LD + q];
       s2 += stage[(i + 2) * LD + p] * stage[(i + 2) * LD + q];
@@ -90,7 +93,7 @@ __device__ void cta_gram(const double* stage, int r, double* dst, double* slots,
   if (!multi) return;
   grid.sync();
   if (blockIdx.x == 0) {
-    for (int e = threadIdx.x; e < r * r; e += TPB) {
+    for (int e = threadIdx.x; e < r * r; e += nt) {
       const int p = e / r, q = e % r;
       if (p > q) continue;
       double s = 0.0;
@@ -130,7 +133,7 @@ __global__ void __launch_bounds__(TPB) nnls_kernel(NnlsLaunch a) {
   double* slots_gram = a.scratch + 3072;
 
   // ---- G: Hadamard of the other modes' Grams (ones, ascending modes).
-  for (int e = threadIdx.x; e < RP * RP; e += TPB) {
+  for (int e = threadIdx.x; e < RP * RP; e += blockDim.x) {
     const int p = e / RP, q = e % RP;
     double g = 0.0;
     if (p < r && q < r) {
@@ -157,30 +160,69 @@ __global__ void __launch_bounds__(TPB) nnls_kernel(NnlsLaunch a) {
   for (int l = 0; l < RP; ++l) W[l] = (valid && l < r) ? w0[(long long)row * r + l] : 0.0;
 
   // ---- AHALS sweeps.
+  // Column j of a pass needs prod_j = (W G)[row, j] with columns < j already
+  // updated in this pass (nnls.cpp:22). It is assembled as
+  //   P[j] = sum_{l >= j} W_old[l] G[l][j]      (all j at once, ILP)
+  //        + sum_{l < j}  W_new[l] G[l][j]      (added as columns finish),
+  // so the serial chain from column j-1 to j is one FMA, not a dot product.
+  // The division by G_jj is a multiply by its reciprocal (<= 1 ulp apart).
+  double* Ginv = stage;  // RP reciprocals (stage is free until the Grams)
+  for (int j = threadIdx.x; j < RP; j += blockDim.x) Ginv[j] = (j < r && Gs[j * RP + j] > 0.0) ? 1.0 / Gs[j * RP + j] : 0.0;
+  __syncthreads();
   double first = -1.0;
   int s = 0;
+  constexpr bool kIncremental = RP <= 24;  // P[] costs RP more registers
   for (; s < max_iters; ++s) {
+    double P[kIncremental ? RP : 1];
+    if constexpr (kIncremental) {
+      // row l of G is contiguous: 16-byte broadcast reads, P[j] still sums
+      // l = j, j+1, ... in ascending order
+#pragma unroll
+      for (int j = 0; j < RP; ++j) P[j] = 0.0;
+#pragma unroll
+      for (int l = 0; l < RP; ++l) {
+#pragma unroll
+        for (int j = 0; j <= l; j += 2) {
+          const double2 g = *reinterpret_cast<const double2*>(&Gs[l * RP + j]);
+          P[j] = fma(W[l], g.x, P[j]);
+          if (j + 1 <= l) P[j + 1] = fma(W[l], g.y, P[j + 1]);
+        }
+      }
+    }
     double d2 = 0.0;
 #pragma unroll
     for (int j = 0; j < RP; ++j) {
       if (j < r) {
         const double gjj = Gs[j * RP + j];
-        if (gjj > diag_floor) {
+        double prod;
+        if constexpr (kIncremental) {
+          prod = P[j];
+        } else {
           double p0 = 0.0, p1 = 0.0, p2 = 0.0, p3 = 0.0;
 #pragma unroll
           for (int l = 0; l < RP; l += 4) {
             p0 = fma(W[l + 0], Gs[(l + 0) * RP + j], p0);
-            if (l + 1 < RP) p1 = fma(W[l + 1], Gs[(l + 1) * RP + j], p1);
-            if (l + 2 < RP) p2 = fma(W[l + 2], Gs[(l + 2) * RP + j], p2);
-            if (l + 3 < RP) p3 = fma(W[l + 3], Gs[(l + 3) * RP + j], p3);
+            p1 = fma(W[l + 1], Gs[(l + 1) * RP + j], p1);
+            p2 = fma(W[l + 2], Gs[(l + 2) * RP + j], p2);
+            p3 = fma(W[l + 3], Gs[(l + 3) * RP + j], p3);
           }
-          const double prod = (p0 + p1) + (p2 + p3);
+          prod = (p0 + p1) + (p2 + p3);
+        }
+        if (gjj > diag_floor) {
           const double c = valid ? __ldg(&C[(long long)row * r + j]) : 0.0;
           const double numer = __dadd_rn(__dsub_rn(c, prod), __dmul_rn(gjj, W[j]));
-          const double nw = clip0(__ddiv_rn(numer, gjj));
+          const double nw = clip0(__dmul_rn(numer, Ginv[j]));
           const double d = nw - W[j];
           d2 = fma(d, d, d2);
           W[j] = nw;
+        }
+        if constexpr (kIncremental) {
+#pragma unroll
+          for (int q = (j + 1) & ~1; q < RP; q += 2) {
+            const double2 g = *reinterpret_cast<const double2*>(&Gs[j * RP + q]);
+            if (q > j) P[q] = fma(W[j], g.x, P[q]);
+            P[q + 1] = fma(W[j], g.y, P[q + 1]);
+          }
         }
       }
     }
@@ -193,48 +235,47 @@ __global__ void __launch_bounds__(TPB) nnls_kernel(NnlsLaunch a) {
   }
 
   if (a.role == 2) {
-    if (valid)
-      for (int l = 0; l < r; ++l) a.w_out[(long long)row * r + l] = W[l];
+    if (valid) {
+#pragma unroll
+      for (int l = 0; l < RP; ++l)
+        if (l < r) a.w_out[(long long)row * r + l] = W[l];
+    }
     if (blockIdx.x == 0 && threadIdx.x == 0 && a.sweeps_out) *a.sweeps_out = s;
     return;
   }
 
-  // ---- write the block (HER: solved + extrapolated twin; AO: in place).
-  double* S = F->x[mode][sel ^ 1];
-  float* X32 = F->x32[mode][sel];
-  float* S32 = F->x32[mode][sel ^ 1];
-  double H[RP];
-#pragma unroll
-  for (int l = 0; l < RP; ++l) {
-    double h = W[l];
-    if (a.role == 0 && valid && l < r) {
-      const double old = X[(long long)row * r + l];
-      h = clip0(__dadd_rn(W[l], __dmul_rn(beta, __dsub_rn(W[l], old))));
-    }
-    H[l] = h;
-  }
-  if (valid) {
-    for (int l = 0; l < r; ++l) {
-      const long long o = (long long)row * r + l;
-      X[o] = H[l];
-      if (X32) X32[o] = float(H[l]);
-      if (a.role == 0) {
-        S[o] = W[l];
-        if (S32) S32[o] = float(W[l]);
-      }
-    }
-  }
-
-  // ---- Grams: gram(W) always (needed by F-hat / f), gram(hat) for HER.
+  // ---- Gram(W): needed by F-hat / f and, on a restart, as the new Gram.
 #pragma unroll
   for (int l = 0; l < RP; ++l) stage[threadIdx.x * LD + l] = (valid && l < r) ? W[l] : 0.0;
   __syncthreads();
   double* gW = (a.role == 0) ? F->gram[mode][sel ^ 1] : F->gram[mode][sel];
   cta_gram<RP, TPB>(stage, r, gW, slots_gram, grid);
   __syncthreads();
-  if (a.role == 0) {
+
+  // ---- write the block (HER: solved + extrapolated twin; AO: in place);
+  // the twin is staged for its Gram as it is produced.
+  double* S = F->x[mode][sel ^ 1];
+  float* X32 = F->x32[mode][sel];
+  float* S32 = F->x32[mode][sel ^ 1];
 #pragma unroll
-    for (int l = 0; l < RP; ++l) stage[threadIdx.x * LD + l] = (valid && l < r) ? H[l] : 0.0;
+  for (int l = 0; l < RP; ++l) {
+    double h = 0.0;
+    if (valid && l < r) {
+      const long long o = (long long)row * r + l;
+      if (a.role == 0) {
+        const double old = X[o];
+        h = clip0(__dadd_rn(W[l], __dmul_rn(beta, __dsub_rn(W[l], old))));
+        S[o] = W[l];
+        if (S32) S32[o] = float(W[l]);
+      } else {
+        h = W[l];
+      }
+      X[o] = h;
+      if (X32) X32[o] = float(h);
+    }
+    if (a.role == 0) stage[threadIdx.x * LD + l] = h;
+  }
+  if (a.role == 0) {
     __syncthreads();
     cta_gram<RP, TPB>(stage, r, F->gram[mode][sel], slots_gram, grid);
     __syncthreads();
@@ -246,8 +287,11 @@ __global__ void __launch_bounds__(TPB) nnls_kernel(NnlsLaunch a) {
 
   // ---- objective at the (mixed) point: <W, C> and <W^T W, G>.
   double cross = 0.0;
-  if (valid)
-    for (int l = 0; l < r; ++l) cross += W[l] * C[(long long)row * r + l];
+  if (valid) {
+#pragma unroll
+    for (int l = 0; l < RP; ++l)
+      if (l < r) cross += W[l] * C[(long long)row * r + l];
+  }
   cross = grid_sum<TPB>(cross, red, slots_cross, grid);
   if (gridDim.x > 1) grid.sync();  // gram written by CTA 0 is visible to all
   if (blockIdx.x != 0 || threadIdx.x != 0) return;
@@ -263,7 +307,8 @@ __global__ void __launch_bounds__(TPB) nnls_kernel(NnlsLaunch a) {
   TraceEntry rec;
   rec.f = f;
   rec.time_s = time_s;
-  rec.pad = 0;
+  rec.sweeps = 0;
+  for (int j = 0; j < a.order; ++j) rec.sweeps += st->last_sweeps[j];
   if (a.role == 0) {
     const bool restarted = f > st->f_prev;  // strict (her.cpp:75)
     if (restarted)
@@ -300,7 +345,8 @@ void launch_rp(const NnlsLaunch& a, cudaStream_t s) {
   void* params[] = {&args};
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(TPB);
+  // a single CTA runs exactly the warps its rows need
+  cfg.blockDim = dim3(grid == 1 ? unsigned((a.rows + 31) / 32 * 32) : unsigned(TPB));
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
@@ -318,13 +364,13 @@ void launch_nnls(const NnlsLaunch& a, cudaStream_t s) {
   if (r < 1 || r > kMaxRank) throw Unsupported("rank outside the fused NNLS kernel's range (1..64)");
   if (r <= 4) return launch_rp<4, 512>(a, s);
   if (r <= 8) return launch_rp<8, 512>(a, s);
-  if (r <= 12) return launch_rp<12, 512>(a, s);
-  if (r <= 16) return launch_rp<16, 512>(a, s);
-  if (r <= 20) return launch_rp<20, 512>(a, s);
+  if (r <= 12) return launch_rp<12, 384>(a, s);
+  if (r <= 16) return launch_rp<16, 384>(a, s);
+  if (r <= 20) return launch_rp<20, 384>(a, s);
   if (r <= 24) return launch_rp<24, 256>(a, s);
   if (r <= 32) return launch_rp<32, 256>(a, s);
-  if (r <= 48) return launch_rp<48, 256>(a, s);
-  return launch_rp<64, 256>(a, s);
+  if (r <= 48) return launch_rp<48, 128>(a, s);
+  return launch_rp<64, 128>(a, s);
 }
 
 }  // namespace ntfb

@@ -1,0 +1,32 @@
+// FP32 instantiations of the fast MTTKRP kernel (FFMA on CUDA cores; the
+// per-CTA partials are written in FP64 and reduced in FP64).
+#include "mttkrp_fast_impl.cuh"
+#include "mttkrp_fast_launch.h"
+
+namespace ntfb {
+namespace fast {
+
+template <typename T, int G, int B, int A, int LAYOUT>
+void launch_impl32(const CUtensorMap& map, const Params& p, int grid, int threads, size_t smem, cudaStream_t s) {
+  auto fn = mttkrp_fast_kernel<T, G, B, A, LAYOUT>;
+  NTF_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  fn<<<grid, threads, smem, s>>>(map, p);
+  NTF_CUDA(cudaGetLastError());
+}
+
+#define NTF_CFG32(G, B, A) KernelCfg{G, B, A, launch_impl32<float, G, B, A, kRow>, launch_impl32<float, G, B, A, kCol>}
+
+bool lookup_f32(int r, long long, KernelCfg* out) {
+  if (r <= 4) *out = NTF_CFG32(2, 2, 4);
+  else if (r <= 8) *out = NTF_CFG32(2, 4, 4);
+  else if (r <= 12) *out = NTF_CFG32(2, 6, 4);
+  else if (r <= 16) *out = NTF_CFG32(2, 8, 4);
+  else if (r <= 20) *out = NTF_CFG32(4, 5, 4);
+  else if (r <= 32) *out = NTF_CFG32(4, 8, 4);
+  else if (r <= 64) *out = NTF_CFG32(8, 8, 8);
+  else return false;
+  return true;
+}
+
+}  // namespace fast
+}  // namespace ntfb

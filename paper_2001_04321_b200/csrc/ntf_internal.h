@@ -69,7 +69,7 @@ struct RunState {
 
 struct TraceEntry {
   double f, beta, time_s;
-  int restarted, pad;
+  int restarted, sweeps;
 };
 
 // Mode view (L, I, R) of the LOCAL slab (kernels.cpp:10-27); dims[0] is the

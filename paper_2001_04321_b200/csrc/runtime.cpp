@@ -9,6 +9,7 @@
 #include <string>
 
 #include "mttkrp_fast.h"
+#include "mttkrp_fast_launch.h"
 
 namespace ntfb {
 
@@ -104,6 +105,12 @@ MttkrpEngine::MttkrpEngine(const ntf_ctx* ctx, const ntf_tensor* t, int rank, un
     slab_meta_ = DevBuf(meta.size() * sizeof(long long));
     NTF_CUDA(cudaMemcpy(slab_meta_.p, meta.data(), meta.size() * sizeof(long long), cudaMemcpyHostToDevice));
   }
+}
+
+std::string MttkrpEngine::describe(int mode) const {
+  const ModeView v = view(mode);
+  if (!(flags_ & NTF_RUN_GENERIC) && fast_mttkrp_supported(v, t_->dtype)) return fast_mttkrp_describe(v, t_->dtype, ctx_->sms);
+  return "generic segs=" + std::to_string(segs_[mode]);
 }
 
 int MttkrpEngine::kernels_per_call(int mode) const {
@@ -352,6 +359,7 @@ void Session::trace(double* f0, ntf_trace_record* out, int cap, int* n) {
     r.iter = i + 1;
     r.time_s = tr[size_t(i)].time_s;
     r.f = tr[size_t(i)].f;
+    r.inner_sweeps = tr[size_t(i)].sweeps;
     if (algo_ == 0) {
       r.has_restarted = 1;
       r.restarted = tr[size_t(i)].restarted;

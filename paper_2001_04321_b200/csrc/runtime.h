@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <memory>
+#include <string>
 #include <vector>
 
 #include "ntf_internal.h"
@@ -60,6 +61,7 @@ class MttkrpEngine {
            cudaEvent_t ev1 = nullptr);
   int kernels_per_call(int mode) const;
   ModeView view(int mode) const;
+  std::string describe(int mode) const;
 
  private:
   const ntf_ctx* ctx_;
