@@ -639,6 +639,15 @@ int ntf_session_kernel_times(ntf_session* s, double* ms_per_mode, int* launches_
   });
 }
 
+// Diagnostics (not part of the public header): CTA-0 cycle counters of the
+// NNLS kernel {sweep-loop cycles, reduction cycles, sweeps, calls}.
+int ntf_debug_nnls_prof(unsigned long long* out, int reset) {
+  return guarded([&] {
+    need(out, "out");
+    nnls_prof_read(out, reset != 0);
+  });
+}
+
 int ntf_session_destroy(ntf_session* s) {
   return guarded([&] { delete SESSION(s); });
 }

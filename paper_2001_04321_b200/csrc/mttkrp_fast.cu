@@ -4,6 +4,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 
 #include "mttkrp_fast.h"
@@ -52,26 +53,42 @@ bool choose(const ModeView& v, int dtype, int sms, Choice* out) {
   } else {
     return false;
   }
+  // the producer bulk-copies KB consecutive rows of the last varying mode's
+  // factor per unit (rows of r elements must be 16-byte multiples) and
+  // assumes at most one wrap of that digit inside a unit
+  const int kb = int(128 / es);
+  if ((v.rank * es) % 16) return false;
+  const int qL = layout == fast::kRow ? v.order - 1 : v.order - 2;
+  if (v.dims[qL] < kb) return false;
+  if (v.order > fast::kMaxBase + 2) return false;  // base rows per unit <= kMaxBase
   fast::KernelCfg cfg;
   if (!fast::lookup(dtype, v.rank, v.I, &cfg)) return false;
   const int RW = (32 / cfg.G) * cfg.A;
   const long long mw_total = (v.I + RW - 1) / RW;
+  const int warp_cap = fast::max_threads(cfg.A, cfg.B) / 32;
+  int NP = 2;  // producer warps (each forms W for every NP-th unit)
+  if (const char* e = std::getenv("NTF_FAST_NP")) NP = std::max(1, std::atoi(e));  // tuning override
+  const int cons_cap = std::min(kMaxMW, warp_cap - NP);
+  if (cons_cap < 1) return false;
   int MW, n_mtiles;
-  if (mw_total <= kMaxMW) {
+  if (mw_total <= cons_cap) {
     MW = int(mw_total);
     n_mtiles = 1;
   } else {
-    MW = 8;
-    n_mtiles = int((v.I + 8LL * RW - 1) / (8LL * RW));
+    MW = std::min(cons_cap, 8);
+    n_mtiles = int((v.I + (long long)MW * RW - 1) / ((long long)MW * RW));
   }
-  const int KW = std::max(1, std::min(8, 8 / MW));
+  // at least four consumer warps (one per SM sub-partition): split k
+  int KW = std::max(1, std::min(8, (4 + MW - 1) / MW));
+  if (const char* e = std::getenv("NTF_FAST_KW")) KW = std::max(1, std::min(8, std::atoi(e)));
+  while (MW * KW > cons_cap && KW > 1) --KW;
   const int m_cta = MW * RW;
   fast::Params& p = out->p;
   p = fast::Params{};
   p.v = v;
   p.MW = MW;
   p.KW = KW;
-  p.NP = std::max(1, std::min(2, 12 - MW * KW));
+  p.NP = NP;
   p.m_cta = m_cta;
   p.n_mbox = (m_cta + 255) / 256;
   p.m_box = m_cta / p.n_mbox;
@@ -92,9 +109,17 @@ bool choose(const ModeView& v, int dtype, int sms, Choice* out) {
   }
   p.tx_bytes = p.t_stage_bytes;
   p.w_stage_bytes = unsigned((size_t(p.kbox) * p.wld * es + 127) / 128 * 128);
-  const size_t per_stage = size_t(p.t_stage_bytes) + p.w_stage_bytes;
+  // KB rows of the last varying mode, 2 x kMaxBase base rows, 2 info ints
+  p.aq_stage_bytes = unsigned(((size_t(p.kbox) + 2 * fast::kMaxBase) * v.rank * es + 2 * sizeof(int) + 127) / 128 * 128);
+  const size_t per_stage = size_t(p.t_stage_bytes) + p.w_stage_bytes + p.aq_stage_bytes;
   p.stages = int(std::min<size_t>(8, kSmemBudget / per_stage));
-  if (p.stages < 2) return false;
+  if (const char* e = std::getenv("NTF_FAST_STAGES"))  // tuning override
+    p.stages = std::min(p.stages, std::max(2, std::atoi(e)));
+  // Producer warp w owns stages s == w (mod NP) and visits them in
+  // consecutive rounds, so its parity waits never run more than one phase
+  // ahead of an mbarrier; that needs NP | stages.
+  p.stages -= p.stages % p.NP;
+  if (p.stages < 2 * p.NP) return false;  // each producer looks at least one unit ahead
   // the k-split fold reuses the T stages as scratch
   if (size_t(m_cta) * cfg.G * cfg.B * es > size_t(p.stages) * p.t_stage_bytes) return false;
   p.ctas_per_mtile = int(std::max<long long>(1, std::min<long long>(p.units, std::max(1, sms / n_mtiles))));
@@ -102,7 +127,7 @@ bool choose(const ModeView& v, int dtype, int sms, Choice* out) {
   out->layout = layout;
   out->grid = n_mtiles * p.ctas_per_mtile;
   out->threads = 32 * (p.NP + MW * KW);
-  out->smem = size_t(p.stages) * per_stage + 2 * size_t(p.stages) * sizeof(uint64_t);
+  out->smem = size_t(p.stages) * per_stage + 3 * size_t(p.stages) * sizeof(uint64_t);
   return true;
 }
 
@@ -156,16 +181,127 @@ size_t fast_mttkrp_partial_len(const ModeView& v, int dtype, int sms) {
   return size_t(ch.p.ctas_per_mtile) * v.I * v.rank;
 }
 
-void fast_mttkrp(const void* t, int dtype, const ModeView& v, const DevFactors* dF, double* partial, double* out,
-                 int sms, cudaStream_t s) {
+namespace {
+
+// Modes whose digit varies with k inside a unit (ROW: after `mode`; COL:
+// before it), the last of them (qL, fastest), and the base modes (every
+// other contributing mode, ascending).
+struct UnitModes {
+  bool vary[kMaxOrder] = {}, fixd[kMaxOrder] = {};
+  int qL = 0, nb = 0, bq[fast::kMaxBase] = {};
+};
+
+UnitModes unit_modes(const ModeView& v, int layout) {
+  UnitModes m;
+  for (int q = 0; q < v.order; ++q) {
+    m.vary[q] = layout == fast::kRow ? q > v.mode : q < v.mode;
+    m.fixd[q] = layout == fast::kRow && q < v.mode;
+  }
+  m.qL = layout == fast::kRow ? v.order - 1 : v.order - 2;
+  for (int q = 0; q < v.order; ++q)
+    if ((m.vary[q] || m.fixd[q]) && q != m.qL) m.bq[m.nb++] = q;
+  return m;
+}
+
+void fill_params_modes(const ModeView& v, int layout, fast::Params& p) {
+  const UnitModes m = unit_modes(v, layout);
+  p.qL = m.qL;
+  p.nb = m.nb;
+  for (int t = 0; t < fast::kMaxBase; ++t) p.bq[t] = m.bq[t];
+  p.rowL_wrap = m.qL == 0 ? int(v.row0) : 0;
+}
+
+}  // namespace
+
+std::vector<int> fast_mttkrp_unit_table(const ModeView& v, int dtype, int sms) {
+  Choice ch;
+  if (!choose(v, dtype, sms, &ch)) return {};
+  const UnitModes m = unit_modes(v, ch.layout);
+  const fast::Params& p = ch.p;
+  const int kb = p.kbox;
+  std::vector<int> tab(size_t(p.units) * fast::kUnitInts, 0);
+  for (long long u = 0; u < p.units; ++u) {
+    int* e = &tab[size_t(u) * fast::kUnitInts];
+    long long l, first, kmax;
+    if (ch.layout == fast::kRow) {
+      l = u / p.nbox_r;
+      first = (u - l * p.nbox_r) * kb;
+      kmax = v.R - first;
+      e[0] = int(first);
+      e[1] = int(l);
+    } else {
+      l = 0;
+      first = u * kb;
+      kmax = v.L - first;
+      e[0] = int(first);
+      e[1] = 0;
+    }
+    int dig[kMaxOrder] = {};
+    long long rem = first, lrem = l;
+    for (int q = v.order - 1; q >= 0; --q) {
+      if (m.vary[q]) {
+        dig[q] = int(rem % v.dims[q]);
+        rem /= v.dims[q];
+      } else if (m.fixd[q]) {
+        dig[q] = int(lrem % v.dims[q]);
+        lrem /= v.dims[q];
+      }
+    }
+    const int dimL = v.dims[m.qL];
+    const int n_valid = int(std::min<long long>(kb, kmax));
+    e[2] = dig[m.qL] + (m.qL == 0 ? int(v.row0) : 0);
+    e[3] = n_valid;
+    e[4] = std::min(n_valid, dimL - dig[m.qL]);
+    e[5] = dimL - dig[m.qL];
+    for (int t = 0; t < m.nb; ++t) e[6 + t] = dig[m.bq[t]] + (m.bq[t] == 0 ? int(v.row0) : 0);
+    // carry of the wrap into the higher varying digits
+    bool carry = true;
+    for (int q = v.order - 1; q >= 0; --q)
+      if (m.vary[q] && q < m.qL && carry) {
+        if (++dig[q] < v.dims[q])
+          carry = false;
+        else
+          dig[q] = 0;
+      }
+    for (int t = 0; t < m.nb; ++t) e[6 + fast::kMaxBase + t] = dig[m.bq[t]] + (m.bq[t] == 0 ? int(v.row0) : 0);
+  }
+  return tab;
+}
+
+void fast_mttkrp(const void* t, int dtype, const ModeView& v, const DevFactors* dF, const int* unit_table,
+                 double* partial, double* out, int sms, cudaStream_t s) {
   Choice ch;
   if (!choose(v, dtype, sms, &ch)) throw Unsupported("no fast MTTKRP plan for this view");
+  if (!unit_table) throw LogicError("fast MTTKRP needs its unit table");
   CUtensorMap map;
   make_map(t, dtype, v, ch, &map);
   ch.p.F = dF;
   ch.p.partial = partial;
+  ch.p.utab = unit_table;
+  fill_params_modes(v, ch.layout, ch.p);
+  // diagnostics: NTF_FAST_PROF=1 prints per-CTA-averaged pipeline wait cycles
+  static unsigned long long* prof = nullptr;
+  const bool profiling = std::getenv("NTF_FAST_PROF") != nullptr;
+  if (profiling) {
+    const size_t n = size_t(ch.grid) * fast::kProfSlots;
+    if (!prof) NTF_CUDA(cudaMalloc(&prof, 4096 * fast::kProfSlots * sizeof(unsigned long long)));
+    NTF_CUDA(cudaMemsetAsync(prof, 0, n * sizeof(unsigned long long), s));
+    ch.p.prof = prof;
+  }
   fast::LaunchFn fn = ch.layout == fast::kRow ? ch.cfg.row : ch.cfg.col;
   fn(map, ch.p, ch.grid, ch.threads, ch.smem, s);
+  if (profiling) {
+    std::vector<unsigned long long> h(size_t(ch.grid) * fast::kProfSlots);
+    NTF_CUDA(cudaMemcpyAsync(h.data(), prof, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    NTF_CUDA(cudaStreamSynchronize(s));
+    double a[fast::kProfSlots] = {};
+    for (int b = 0; b < ch.grid; ++b)
+      for (int q = 0; q < fast::kProfSlots; ++q) a[q] += double(h[size_t(b) * fast::kProfSlots + q]) / ch.grid;
+    fprintf(stderr,
+            "[fast-prof mode %d] units/CTA %.1f | producer %.0f cyc (stage wait %.0f, copy wait %.0f) | "
+            "consumer %.0f cyc (data wait %.0f) | %.0f cyc/unit\n",
+            v.mode, a[5], a[0], a[1], a[2], a[3], a[4], a[5] > 0 ? a[3] / a[5] : 0.0);
+  }
   launch_reduce_partials(partial, ch.p.ctas_per_mtile, v.I * v.rank, out, s);
 }
 

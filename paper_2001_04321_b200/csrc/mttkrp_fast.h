@@ -2,6 +2,8 @@
 // rows, register-blocked CUDA-core FMA, deterministic split-K reduction).
 #pragma once
 
+#include <vector>
+
 #include "ntf_internal.h"
 
 namespace ntfb {
@@ -13,7 +15,11 @@ int fast_mttkrp_kernels(const ModeView& v, int dtype);
 // Doubles of split-K workspace the fast path needs for this view.
 size_t fast_mttkrp_partial_len(const ModeView& v, int dtype, int sms);
 // out = MTTKRP (I x r, FP64) of the local view.
-void fast_mttkrp(const void* t, int dtype, const ModeView& v, const DevFactors* dF, double* partial, double* out,
+// Host-built per-unit table of the fast path (see mttkrp_fast_launch.h);
+// empty when the view has no fast plan. Depends only on shape and dtype.
+std::vector<int> fast_mttkrp_unit_table(const ModeView& v, int dtype, int sms);
+void fast_mttkrp(const void* t, int dtype, const ModeView& v, const DevFactors* dF, const int* unit_table,
+                 double* partial, double* out,
                  int sms, cudaStream_t s);
 
 }  // namespace ntfb

@@ -1,4 +1,6 @@
 // FP64 instantiations of the fast MTTKRP kernel (DFMA on CUDA cores).
+#include <cstdlib>
+
 #include "mttkrp_fast_impl.cuh"
 #include "mttkrp_fast_launch.h"
 
@@ -15,15 +17,25 @@ void launch_impl(const CUtensorMap& map, const Params& p, int grid, int threads,
 
 #define NTF_CFG(T, G, B, A) KernelCfg{G, B, A, launch_impl<T, G, B, A, kRow>, launch_impl<T, G, B, A, kCol>}
 
+// Blocking per rank. Shared-memory bytes per DFMA are 8 (A + B) / (A B)
+// (T and W values delivered per lane), and the SM moves 128 B/clk against 64
+// DFMA/clk, so the production shapes keep A*B/(A+B) near 5 (C2: 10x10,
+// C3: 7x8) and split k across warps to keep four consumer warps.
 bool lookup_f64(int r, long long rows, KernelCfg* out) {
+  if (const char* e = std::getenv("NTF_FAST_ALT")) {  // tuning: alternative blockings
+    const int alt = std::atoi(e);
+    if (r > 16 && r <= 20 && alt == 1) return *out = NTF_CFG(double, 2, 10, 5), true;
+    if (r > 16 && r <= 20 && alt == 2) return *out = NTF_CFG(double, 4, 5, 8), true;
+    if (r > 12 && r <= 16 && alt == 1) return *out = NTF_CFG(double, 2, 8, 4), true;
+  }
   if (r <= 4) *out = NTF_CFG(double, 2, 2, 2);
-  else if (r <= 8) *out = NTF_CFG(double, 2, 4, 2);
-  else if (r <= 10) *out = NTF_CFG(double, 2, 5, 2);
-  else if (r <= 12) *out = NTF_CFG(double, 2, 6, 2);
-  else if (r <= 16) *out = (rows > 64 && rows <= 112) ? NTF_CFG(double, 4, 4, 14) : NTF_CFG(double, 2, 8, 2);
-  else if (r <= 20) *out = NTF_CFG(double, 4, 5, 4);
-  else if (r <= 24) *out = NTF_CFG(double, 4, 6, 4);
-  else if (r <= 32) *out = NTF_CFG(double, 4, 8, 4);
+  else if (r <= 8) *out = NTF_CFG(double, 2, 4, 4);
+  else if (r <= 10) *out = NTF_CFG(double, 2, 5, 4);
+  else if (r <= 12) *out = NTF_CFG(double, 2, 6, 6);
+  else if (r <= 16) *out = (rows > 64 && rows <= 112) ? NTF_CFG(double, 2, 8, 7) : NTF_CFG(double, 2, 8, 8);
+  else if (r <= 20) *out = NTF_CFG(double, 2, 10, 10);
+  else if (r <= 24) *out = NTF_CFG(double, 2, 12, 8);
+  else if (r <= 32) *out = NTF_CFG(double, 4, 8, 8);
   else if (r <= 64) *out = NTF_CFG(double, 8, 8, 8);
   else return false;
   return true;

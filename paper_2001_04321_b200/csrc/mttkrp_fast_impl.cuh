@@ -33,6 +33,10 @@
 #include "mttkrp_fast_launch.h"
 #include "ntf_internal.h"
 
+#ifndef NTF_FAST_PROFILE
+#define NTF_FAST_PROFILE 0
+#endif
+
 namespace ntfb {
 namespace fast {
 
@@ -59,6 +63,17 @@ __device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
 }
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t tx) {
   asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(b)), "r"(tx) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* b, uint32_t tx) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(b)), "r"(tx)
+               : "memory");
+}
+// 1-D bulk copy global -> shared (16-byte aligned, size a multiple of 16).
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_addr(dst)),
+               "l"(src), "r"(bytes), "r"(smem_addr(bar))
+               : "memory");
 }
 __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
   asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_addr(b)) : "memory");
@@ -95,14 +110,13 @@ __device__ __forceinline__ const float* factor_ptr<float>(const DevFactors* F, i
 // G column groups of B columns each (padded to BP so 16-byte loads stay
 // aligned); RG = 32/G row groups; A rows per lane.
 template <typename T, int G, int B, int A, int LAYOUT>
-__global__ void __launch_bounds__(384, 1) mttkrp_fast_kernel(const __grid_constant__ CUtensorMap tmap, Params p) {
+__global__ void __launch_bounds__(max_threads(A, B), 1) mttkrp_fast_kernel(const __grid_constant__ CUtensorMap tmap, Params p) {
   using VT = Vec<T>;
   using V = typename VT::V;
   constexpr int VEC = VT::N;
   constexpr int RG = 32 / G;
   constexpr int BP = (B + VEC - 1) / VEC * VEC;
   constexpr int NV = BP / VEC;
-  static_assert(LAYOUT == kRow || A % VEC == 0, "COL layout reads VEC consecutive rows");
 
   extern __shared__ __align__(1024) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -111,9 +125,11 @@ __global__ void __launch_bounds__(384, 1) mttkrp_fast_kernel(const __grid_consta
   const int stages = p.stages;
   unsigned char* t_base = smem;
   T* w_base = reinterpret_cast<T*>(smem + size_t(stages) * p.t_stage_bytes);
-  uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(w_base) +
-                                               size_t(stages) * p.w_stage_bytes);
+  T* aq_base = reinterpret_cast<T*>(reinterpret_cast<unsigned char*>(w_base) + size_t(stages) * p.w_stage_bytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(aq_base) +
+                                               size_t(stages) * p.aq_stage_bytes);
   uint64_t* empty = full + stages;
+  uint64_t* aqb = empty + stages;  // factor rows of a unit landed (producer-only)
 
   const int mt = blockIdx.x / p.ctas_per_mtile;
   const int j = blockIdx.x % p.ctas_per_mtile;
@@ -121,11 +137,14 @@ __global__ void __launch_bounds__(384, 1) mttkrp_fast_kernel(const __grid_consta
   const long long u1 = p.units * (j + 1) / p.ctas_per_mtile;
   const int n_consumers = p.MW * p.KW;
   const int NP = p.NP;  // producer warps
+  // diagnostics only: compiled in with -DNTF_FAST_PROFILE=1
+  const bool prof_on = NTF_FAST_PROFILE && p.prof != nullptr;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < stages; ++s) {
       mbar_init(&full[s], 32);
       mbar_init(&empty[s], n_consumers);
+      mbar_init(&aqb[s], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap) : "memory");
@@ -142,154 +161,153 @@ __global__ void __launch_bounds__(384, 1) mttkrp_fast_kernel(const __grid_consta
 
   if (warp < NP) {
     // ------------------------------------------------------------ producer
-    // Lane owns columns c = lane (+32); the k-varying modes (ROW: modes after
-    // `mode`, i.e. rho; COL: all modes before it, i.e. l) advance as an
-    // odometer, so a unit costs KB x (#varying modes) coalesced row loads per
-    // lane, all independent, and no integer division inside the k loop.
+    // W[k][c] = base[c] * A_qL[dl0 + k][c]: only the last varying digit
+    // (mode qL) moves between consecutive k of a unit, so the unit's KB rows
+    // of A_qL are consecutive in memory (two runs at a wrap). They arrive
+    // with one or two cp.async.bulk copies issued D units ahead on the aq
+    // barrier; `base` (every other factor row) changes rarely and is an L1
+    // hit. The producer then only multiplies shared-memory rows.
+    // Everything shape-dependent about a unit (TMA coordinates, first row and
+    // wrap of the last varying digit, base-row indices) comes from the
+    // host-built unit table, so the producer does no index arithmetic.
     constexpr int KB = 128 / int(sizeof(T));
     constexpr int CPL = (G * B + 31) / 32;  // columns per lane
-    const T* fac[kMaxOrder];
-    int dims[kMaxOrder];
-    bool vary[kMaxOrder], fixd[kMaxOrder];
+    const T* fL = factor_ptr<T>(p.F, p.qL);
+    const T* bfac[kMaxBase];
 #pragma unroll
-    for (int q = 0; q < kMaxOrder; ++q) {
-      fac[q] = q < v.order ? factor_ptr<T>(p.F, q) : nullptr;
-      dims[q] = q < v.order ? v.dims[q] : 1;
-      vary[q] = q < v.order && (LAYOUT == kRow ? q > v.mode : q < v.mode);
-      fixd[q] = LAYOUT == kRow && q < v.mode;
-    }
-    const int row0 = int(v.row0);
-    // Producer warp `warp` owns the units i = warp, warp + NP, ... of this
-    // CTA's range; unit i lives in stage i % stages during round i / stages.
-    for (long long i = warp; i < u1 - u0; i += NP) {
-      const long long u = u0 + i;
-      const int s = int(i % stages);
-      const uint32_t round = uint32_t(i / stages);
-      if (round > 0) mbar_wait(&empty[s], (round - 1) & 1);
-      long long l, rho0;
-      if (LAYOUT == kRow) {
-        l = u / p.nbox_r;
-        rho0 = (u - l * p.nbox_r) * p.kbox;
-      } else {
-        l = u * p.kbox;
-        rho0 = 0;
-      }
-      unsigned char* ts = t_base + size_t(s) * p.t_stage_bytes;
+    for (int t = 0; t < kMaxBase; ++t) bfac[t] = t < p.nb ? factor_ptr<T>(p.F, p.bq[t]) : nullptr;
+    const unsigned row_bytes = unsigned(r * sizeof(T));
+    // aq stage: [KB rows of A_qL][nb base rows][nb base rows after the wrap]
+    // then two ints (valid k count, first k after the wrap).
+    const int aq_elems = int(p.aq_stage_bytes / sizeof(T));
+    auto aq_of = [&](int s) { return aq_base + size_t(s) * aq_elems; };
+    auto info_of = [&](int s) { return reinterpret_cast<int*>(aq_of(s) + (KB + 2 * kMaxBase) * r); };
+
+    // Producer warp `warp` owns the units i = warp + NP*jj of this CTA's
+    // range; unit i lives in stage i % stages during round i / stages
+    // (NP | stages, so each producer cycles through its own stages).
+    const long long n_units = u1 - u0;
+    const long long n_mine = n_units > warp ? (n_units - warp + NP - 1) / NP : 0;
+    // copies of a unit are issued D units before its W is formed (1 <= D <
+    // stages/NP, so the stage wait in issue() only ever depends on W already
+    // produced: no deadlock)
+    const int D = (stages / NP) / 2 > 1 ? (stages / NP) / 2 : 1;
+    long long pw_empty = 0, pw_aq = 0;  // diagnostics (p.prof)
+    const long long pt0 = prof_on ? clock64() : 0;
+    // Unit-table entries are read by lane 0 one iteration ahead.
+    struct Ent {
+      int e[kUnitInts];
+    };
+    auto fetch = [&](long long jj) {
+      Ent t;
       if (lane == 0) {
+        const int2* src = reinterpret_cast<const int2*>(p.utab + size_t(u0 + warp + jj * NP) * kUnitInts);
+#pragma unroll
+        for (int q = 0; q < kUnitInts / 2; ++q) {
+          const int2 x = __ldg(src + q);
+          t.e[2 * q] = x.x;
+          t.e[2 * q + 1] = x.y;
+        }
+      }
+      return t;
+    };
+    // stage / round of the next unit to issue and to form (NP | stages)
+    int s_is = warp, s_cp = warp;
+    uint32_t r_is = 0, r_cp = 0;
+    auto issue = [&](const Ent& en) {
+      const int s = s_is;
+      if (r_is > 0) {
+        const long long t0 = prof_on ? clock64() : 0;
+        mbar_wait(&empty[s], (r_is - 1) & 1);
+        if (prof_on) pw_empty += clock64() - t0;
+      }
+      if ((s_is += NP) >= stages) {
+        s_is -= stages;
+        ++r_is;
+      }
+      if (lane == 0) {
+        const int* e = en.e;
+        const int n_valid = e[3], n1 = e[4], kwrap = e[5];
+        unsigned char* ts = t_base + size_t(s) * p.t_stage_bytes;
         mbar_expect_tx(&full[s], p.tx_bytes);
         for (int mb = 0; mb < p.n_mbox; ++mb) {
           const int m0 = mt * p.m_cta + mb * p.m_box;
           if (LAYOUT == kRow)
-            tma_load_3d(ts + size_t(mb) * p.m_box * 128, &tmap, &full[s], int(rho0), m0, int(l));
+            tma_load_3d(ts + size_t(mb) * p.m_box * 128, &tmap, &full[s], e[0], m0, e[1]);
           else
-            tma_load_3d(ts + size_t(mb) * p.m_box * p.kbox * sizeof(T), &tmap, &full[s], m0, int(l), 0);
+            tma_load_3d(ts + size_t(mb) * p.m_box * p.kbox * sizeof(T), &tmap, &full[s], m0, e[0], 0);
         }
-      }
-      // Khatri-Rao rows of this unit: W[k][cg*BP + b] for column c = cg*B + b.
-      T* ws = w_base + size_t(s) * (p.w_stage_bytes / sizeof(T));
-      int dig[kMaxOrder];
-      {
-        // l and rho0 are < 2^31 on the fast path (checked by the planner)
-        unsigned rem = unsigned((LAYOUT == kRow) ? rho0 : l);  // digits of the first k
-        unsigned lrem = unsigned(l);                           // ROW: fixed digits of l
+        T* aq = aq_of(s);
+        int* info = info_of(s);
+        info[0] = n_valid;
+        info[1] = kwrap;
+        const bool wrap = kwrap < KB;
+        // this warp's generic reads of the previous use of aq[s] precede the copies
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_arrive_expect_tx(&aqb[s], unsigned(n_valid + p.nb * (wrap ? 2 : 1)) * row_bytes);
+        bulk_load(aq, fL + size_t(e[2]) * r, unsigned(n1) * row_bytes, &aqb[s]);
+        if (n_valid > n1)
+          bulk_load(aq + size_t(n1) * r, fL + size_t(p.rowL_wrap) * r, unsigned(n_valid - n1) * row_bytes, &aqb[s]);
 #pragma unroll
-        for (int q = kMaxOrder - 1; q >= 0; --q) {
-          dig[q] = 0;
-          if (vary[q]) {
-            dig[q] = int(rem % unsigned(dims[q]));
-            rem /= unsigned(dims[q]);
-          } else if (fixd[q]) {
-            dig[q] = int(lrem % unsigned(dims[q]));
-            lrem /= unsigned(dims[q]);
+        for (int t = 0; t < kMaxBase; ++t)
+          if (t < p.nb) {
+            bulk_load(aq + size_t(KB + t) * r, bfac[t] + size_t(e[6 + t]) * r, row_bytes, &aqb[s]);
+            if (wrap)
+              bulk_load(aq + size_t(KB + kMaxBase + t) * r, bfac[t] + size_t(e[6 + kMaxBase + t]) * r, row_bytes,
+                        &aqb[s]);
           }
-        }
       }
-      const long long kmax = (LAYOUT == kRow) ? v.R - rho0 : v.L - l;  // valid k < kmax
-      // Only the last varying digit (mode qL) moves between consecutive k,
-      // except at a wrap: W[k][c] = base[c] * A_qL[dl + k][c] with base the
-      // product of every other factor row, recomputed only after a wrap.
-      const int qL = (LAYOUT == kRow) ? v.order - 1 : v.order - 2;
-      const T* __restrict__ fL = fac[0];
-#pragma unroll
-      for (int q = 1; q < kMaxOrder; ++q)
-        if (q == qL) fL = fac[q];
-      const int offL = (qL == 0) ? row0 : 0;
-      int dimL = dims[0];
-#pragma unroll
-      for (int q = 1; q < kMaxOrder; ++q)
-        if (q == qL) dimL = dims[q];
+    };
+    // Iteration jj issues the copies of unit jj (as soon as its stage is
+    // free) and forms W of unit jj - D, whose copies have had D iterations to
+    // land: W runs up to `stages/NP` units ahead of the consumers.
+    Ent ent = fetch(0);
+    for (long long jj = 0; jj < n_mine + D; ++jj) {
+      if (jj < n_mine) {
+        const Ent ent_next = (jj + 1 < n_mine) ? fetch(jj + 1) : ent;
+        issue(ent);
+        ent = ent_next;
+      }
+      if (jj < D) continue;
+      const int s = s_cp;
+      const uint32_t round = r_cp;
+      if ((s_cp += NP) >= stages) {
+        s_cp -= stages;
+        ++r_cp;
+      }
+      T* ws = w_base + size_t(s) * (p.w_stage_bytes / sizeof(T));
+      const T* aq = aq_of(s);
+      {
+        const long long t0 = prof_on ? clock64() : 0;
+        mbar_wait(&aqb[s], round & 1);
+        if (prof_on) pw_aq += clock64() - t0;
+      }
+      const int* info = info_of(s);
+      const int kmax = info[0];   // valid k < kmax
+      const int kwrap = info[1];  // first k after the wrap of the last varying digit
+      const bool wrap = kwrap < KB;
 #pragma unroll
       for (int ci = 0; ci < CPL; ++ci) {
         const int c = lane + 32 * ci;
         if (c >= r) continue;
-        int d[kMaxOrder];
+        T base0 = T(1), base1 = T(1);
 #pragma unroll
-        for (int q = 0; q < kMaxOrder; ++q) d[q] = dig[q];
-        auto make_base = [&]() {
-          T b = T(1);
-#pragma unroll
-          for (int q = 0; q < kMaxOrder; ++q)
-            if ((fixd[q] || vary[q]) && q != qL) b *= __ldg(&fac[q][(d[q] + (q == 0 ? row0 : 0)) * r + c]);
-          return b;
-        };
-        const T base0 = make_base();
-        int dl0 = 0;
-#pragma unroll
-        for (int q = 0; q < kMaxOrder; ++q)
-          if (q == qL) dl0 = d[q];
+        for (int t = 0; t < kMaxBase; ++t)
+          if (t < p.nb) {
+            base0 *= aq[(KB + t) * r + c];
+            base1 *= aq[(KB + (wrap ? kMaxBase : 0) + t) * r + c];
+          }
         T* dst = ws + (c / B) * BP + (c % B);
-        const int kwrap = dimL - dl0;  // first k whose last digit wraps to 0
-        if (kwrap < KB && dimL < KB) {
-          // tiny last mode (several wraps per unit): plain odometer walk
-          int dl = dl0;
-          T base = base0;
-          for (int k = 0; k < KB; ++k) {
-            const T val = base * __ldg(&fL[(dl + offL) * r + c]);
-            dst[k * p.wld] = (k < kmax) ? val : T(0);
-            if (++dl == dimL) {
-              dl = 0;
-              bool carry = true;
-#pragma unroll
-              for (int q = kMaxOrder - 1; q >= 0; --q) {
-                if (vary[q] && q < qL && carry) {
-                  if (++d[q] < dims[q])
-                    carry = false;
-                  else
-                    d[q] = 0;
-                }
-              }
-              base = make_base();
-            }
-          }
-          continue;
-        }
-        // at most one wrap: base1 (after the carry) is fetched up front and
-        // every factor-row load of the unit is independent of the others
-        T base1 = base0;
-        if (kwrap < KB) {
-          bool carry = true;
-#pragma unroll
-          for (int q = kMaxOrder - 1; q >= 0; --q) {
-            if (vary[q] && q < qL && carry) {
-              if (++d[q] < dims[q])
-                carry = false;
-              else
-                d[q] = 0;
-            }
-          }
-          base1 = make_base();
-        }
-        T row_val[KB];
-#pragma unroll
-        for (int k = 0; k < KB; ++k) {
-          const int row = dl0 + k - (k >= kwrap ? dimL : 0);
-          row_val[k] = __ldg(&fL[(row + offL) * r + c]);
-        }
 #pragma unroll
         for (int k = 0; k < KB; ++k)
-          dst[k * p.wld] = (k < kmax) ? (k >= kwrap ? base1 : base0) * row_val[k] : T(0);
+          dst[k * p.wld] = (k < kmax) ? (k >= kwrap ? base1 : base0) * aq[k * r + c] : T(0);
       }
       mbar_arrive(&full[s]);
+    }
+    if (prof_on && warp == 0 && lane == 0) {
+      p.prof[blockIdx.x * kProfSlots + 0] = clock64() - pt0;
+      p.prof[blockIdx.x * kProfSlots + 1] = pw_empty;
+      p.prof[blockIdx.x * kProfSlots + 2] = pw_aq;
     }
   } else if (warp < NP + n_consumers) {
     // ------------------------------------------------------------ consumers
@@ -303,52 +321,60 @@ __global__ void __launch_bounds__(384, 1) mttkrp_fast_kernel(const __grid_consta
 #pragma unroll
       for (int b = 0; b < B; ++b) acc[i][b] = T(0);
 
+    // Rows owned by the lane. ROW: rg + RG*i. COL: groups of VEC consecutive
+    // rows (one 16-byte read), the last A % VEC rows one by one.
+    constexpr int AV = (A / VEC) * VEC;
+    auto lane_row = [&](int i) {
+      if (LAYOUT == kRow) return mw * RW + rg + RG * i;
+      if (i < AV) return mw * RW + VEC * rg + (i % VEC) + VEC * RG * (i / VEC);
+      return mw * RW + VEC * RG * (A / VEC) + rg + RG * (i - AV);
+    };
     // per-lane smem offsets of its rows (constant over units)
     int off[A];
 #pragma unroll
     for (int i = 0; i < A; ++i) {
-      if (LAYOUT == kRow) {
-        const int m = mw * RW + rg + RG * i;
+      const int m = lane_row(i);
+      if (LAYOUT == kRow)
         off[i] = m;  // row index; byte offset m*128, swizzle key m & 7
-      } else {
-        const int m = mw * RW + VEC * rg + (i % VEC) + VEC * RG * (i / VEC);
+      else
         off[i] = (m / p.m_box) * p.m_box * p.kbox + (m % p.m_box);  // element offset at k = 0
-      }
     }
     int s = 0;
     uint32_t phase = 0;
+    long long cw_full = 0;
+    const long long ct0 = prof_on ? clock64() : 0;
     for (long long u = u0; u < u1; ++u) {
-      mbar_wait(&full[s], phase);
+      {
+        const long long t0 = prof_on ? clock64() : 0;
+        mbar_wait(&full[s], phase);
+        if (prof_on) cw_full += clock64() - t0;
+      }
       const unsigned char* ts = t_base + size_t(s) * p.t_stage_bytes;
       const T* ws = w_base + size_t(s) * (p.w_stage_bytes / sizeof(T)) + cg * BP;
       if (LAYOUT == kRow) {
         constexpr int KCH = 128 / 16;  // 16-byte chunks per 128-byte row
         for (int pc = kw; pc < KCH; pc += p.KW) {
-          T w[VEC][BP];
+          // Shared-memory bandwidth (128 B/clk/SM, every lane receiving its
+          // 16 or 8 bytes even on a broadcast) is the budget: per k a lane
+          // reads B W values and A T values for A*B FMAs, so A and B are
+          // large and the register-heavy tile streams one k at a time.
 #pragma unroll
-          for (int kk = 0; kk < VEC; ++kk)
+          for (int kk = 0; kk < VEC; ++kk) {
+            T w[BP];
 #pragma unroll
             for (int q = 0; q < NV; ++q) {
               const V x = *reinterpret_cast<const V*>(ws + (pc * VEC + kk) * p.wld + q * VEC);
 #pragma unroll
-              for (int e = 0; e < VEC; ++e) w[kk][q * VEC + e] = VT::get(x, e);
+              for (int e = 0; e < VEC; ++e) w[q * VEC + e] = VT::get(x, e);
             }
-          V tv[A];
-#pragma unroll
-          for (int i = 0; i < A; ++i) {
-            const int m = off[i];
-            tv[i] = *reinterpret_cast<const V*>(ts + m * 128 + (((pc ^ m) & 7) << 4));
-          }
-          // kk outermost: an accumulator is reused only after all A*B others
-          // (DFMA latency exceeds a B-long dependency distance)
-#pragma unroll
-          for (int kk = 0; kk < VEC; ++kk)
 #pragma unroll
             for (int i = 0; i < A; ++i) {
-              const T t = VT::get(tv[i], kk);
+              const int m = off[i];
+              const T t = *reinterpret_cast<const T*>(ts + m * 128 + (((pc ^ m) & 7) << 4) + kk * int(sizeof(T)));
 #pragma unroll
-              for (int b = 0; b < B; ++b) acc[i][b] = fma(t, w[kk][b], acc[i][b]);
+              for (int b = 0; b < B; ++b) acc[i][b] = fma(t, w[b], acc[i][b]);
             }
+          }
         }
       } else {
         const T* tt = reinterpret_cast<const T*>(ts);
@@ -370,6 +396,12 @@ __global__ void __launch_bounds__(384, 1) mttkrp_fast_kernel(const __grid_consta
               for (int b = 0; b < B; ++b) acc[i4 * VEC + e][b] = fma(t, w[b], acc[i4 * VEC + e][b]);
             }
           }
+#pragma unroll
+          for (int i = AV; i < A; ++i) {
+            const T t = tt[off[i] + k * p.m_box];
+#pragma unroll
+            for (int b = 0; b < B; ++b) acc[i][b] = fma(t, w[b], acc[i][b]);
+          }
         }
       }
       __syncwarp();
@@ -380,6 +412,11 @@ __global__ void __launch_bounds__(384, 1) mttkrp_fast_kernel(const __grid_consta
       }
     }
 
+    if (prof_on && cw == 0 && lane == 0) {
+      p.prof[blockIdx.x * kProfSlots + 3] = clock64() - ct0;
+      p.prof[blockIdx.x * kProfSlots + 4] = cw_full;
+      p.prof[blockIdx.x * kProfSlots + 5] = u1 - u0;
+    }
     // ------------------------------------------------------------ epilogue
     // k-split warps fold into kw == 0 in kw order through shared memory
     // (the stage buffers are idle once every unit has been consumed).
@@ -390,7 +427,7 @@ __global__ void __launch_bounds__(384, 1) mttkrp_fast_kernel(const __grid_consta
       if (kw == src) {
 #pragma unroll
         for (int i = 0; i < A; ++i) {
-          const int m = (LAYOUT == kRow) ? off[i] : mw * RW + VEC * rg + (i % VEC) + VEC * RG * (i / VEC);
+          const int m = lane_row(i);
 #pragma unroll
           for (int b = 0; b < B; ++b) red[m * ld + cg * B + b] = acc[i][b];
         }
@@ -399,7 +436,7 @@ __global__ void __launch_bounds__(384, 1) mttkrp_fast_kernel(const __grid_consta
       if (kw == 0) {
 #pragma unroll
         for (int i = 0; i < A; ++i) {
-          const int m = (LAYOUT == kRow) ? off[i] : mw * RW + VEC * rg + (i % VEC) + VEC * RG * (i / VEC);
+          const int m = lane_row(i);
 #pragma unroll
           for (int b = 0; b < B; ++b) acc[i][b] += red[m * ld + cg * B + b];
         }
@@ -410,7 +447,7 @@ __global__ void __launch_bounds__(384, 1) mttkrp_fast_kernel(const __grid_consta
       double* out = p.partial + (size_t(j) * v.I) * r;
 #pragma unroll
       for (int i = 0; i < A; ++i) {
-        const int m = (LAYOUT == kRow) ? off[i] : mw * RW + VEC * rg + (i % VEC) + VEC * RG * (i / VEC);
+        const int m = lane_row(i);
         const long long row = (long long)mt * p.m_cta + m;
         if (m < p.m_cta && row < v.I) {
 #pragma unroll

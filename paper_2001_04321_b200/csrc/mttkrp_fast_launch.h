@@ -12,6 +12,20 @@ namespace fast {
 
 enum { kRow = 0, kCol = 1 };
 
+// Unit table: per unit, ints
+//   [0] ROW: rho0 / COL: l0 (TMA coordinate along the reduction)
+//   [1] ROW: l (TMA coordinate of the outer modes)
+//   [2] row of the last varying mode's factor at k = 0 (slab offset included)
+//   [3] valid k count, [4] rows before the wrap of that digit, [5] first k
+//   after the wrap (>= KB when none)
+//   [6, 6+kMaxBase) base rows at k = 0, [6+kMaxBase, 6+2*kMaxBase) after the wrap
+constexpr int kMaxBase = 2;  // fast path: tensors of order <= 4 (others: generic kernel)
+constexpr int kUnitInts = 6 + 2 * kMaxBase;
+// prof slots: [0] producer total, [1] producer waiting for a free stage,
+// [2] producer waiting for its copies, [3] consumer total, [4] consumer
+// waiting for a full stage, [5] units
+constexpr int kProfSlots = 6;
+
 struct Params {
   ModeView v;
   const DevFactors* F;
@@ -21,7 +35,12 @@ struct Params {
   int kbox;         // reduction indices per unit
   int m_box, n_mbox, m_cta, ctas_per_mtile;
   int MW, KW, NP, stages, wld;  // consumer m-warps, k-warps, producer warps
-  unsigned t_stage_bytes, w_stage_bytes, tx_bytes;
+  unsigned t_stage_bytes, w_stage_bytes, aq_stage_bytes, tx_bytes;
+  const int* utab;       // units x kUnitInts (device)
+  int nb;                // base factors per W row
+  int bq[kMaxBase];      // their modes
+  int qL, rowL_wrap;     // last varying mode; its row after a wrap
+  unsigned long long* prof;  // optional per-CTA cycle counters (diagnostics), kProfSlots each
 };
 using LaunchFn = void (*)(const CUtensorMap& map, const Params& p, int grid, int threads, size_t smem,
                           cudaStream_t s);
@@ -31,6 +50,10 @@ struct KernelCfg {
   int G, B, A;
   LaunchFn row, col;
 };
+
+// Thread cap of an instantiation: small accumulator tiles allow 16 warps
+// (<= 128 registers), medium ones 12 warps (<= 168), large 8 (<= 255).
+constexpr int max_threads(int A, int B) { return A * B <= 24 ? 512 : (A * B <= 40 ? 384 : 256); }
 
 // Picks the blocking for (dtype, rank, rows); false when no instantiation
 // covers the rank.

