@@ -82,13 +82,15 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
-// Sum over the cluster without a cluster barrier: every CTA sends its block
-// sum to slot [me] of every CTA with st.async, which completes transaction
-// bytes on the receiver's mbarrier `bar` (expecting n*8 bytes plus its own
-// arrival); the receiver then adds its n slots in CTA-rank order. `phase` is
-// the parity of this use of `bar`. The same bits reach every CTA.
-__device__ double cluster_sum_async(double v, double* red, double* slots, uint64_t* bar, uint32_t phase,
-                                    cg::cluster_group& cl) {
+// Sum over the cluster without a cluster barrier, in two halves so a sweep
+// can run between them: cluster_post sends this CTA's block sum to slot [me]
+// of every CTA with st.async, which completes transaction bytes on the
+// receiver's mbarrier `bar` (expecting n*8 bytes plus its own arrival);
+// cluster_fin waits for the n slots (`phase` = parity of this use of `bar`)
+// and adds them in CTA-rank order. The same bits reach every CTA. A slot
+// buffer is reused two reductions later: a CTA can only post there after
+// every CTA has posted the reduction in between, i.e. after reading it.
+__device__ double cluster_post(double v, double* red, double* slots, uint64_t* bar, cg::cluster_group& cl) {
   const double b = block_sum(v, red);
   const unsigned n = cl.num_blocks();
   if (n == 1) return b;
@@ -105,16 +107,35 @@ __device__ double cluster_sum_async(double v, double* red, double* slots, uint64
                  "l"(__double_as_longlong(b)), "r"(rbar)
                  : "memory");
   }
+  return b;
+}
+
+__device__ double cluster_fin(double b, const double* slots, uint64_t* bar, uint32_t phase, cg::cluster_group& cl) {
+  const unsigned n = cl.num_blocks();
+  if (n == 1) return b;
   asm volatile(
       "{\n\t.reg .pred p;\n"
       "W_%=:\n\t"
-      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
       "@!p bra W_%=;\n}\n" ::"r"(smem_u32(bar)),
       "r"(phase)
       : "memory");
+  // (st.async data is visible once its complete_tx is observed; no
+  // cluster-scope acquire, which would invalidate L1)
   double s = 0.0;
   for (unsigned k = 0; k < n; ++k) s += slots[k];
+  __syncwarp();  // every lane has read the slots before any lane posts again
   return s;
+}
+
+// sqrt(ch2) <= thr (nnls.cpp:38) without the square root on the sweep
+// loop's critical path unless ch2 is within rounding of thr^2.
+__device__ __forceinline__ bool stop_rule(double ch2, double thr) {
+  if (!(thr >= 0.0)) return sqrt(ch2) <= thr;
+  const double t2 = thr * thr;
+  if (ch2 < t2 * (1.0 - 1e-12)) return true;
+  if (ch2 > t2 * (1.0 + 1e-12)) return false;
+  return sqrt(ch2) <= thr;
 }
 
 // Eigen's cwiseMax(0.0): (a < 0) ? 0 : a.
@@ -167,8 +188,9 @@ __global__ void __launch_bounds__(TPB) nnls_kernel(NnlsLaunch a) {
   double* red = Gs + RP * RP;        // 32
   double* pub = red + 32;            // 2 x kMaxCluster: pushed block sums (by parity)
   double* part = pub + 2 * kMaxCluster;  // RP*RP: Gram partial of this CTA
-  double* Ginv = part + RP * RP;     // RP
-  double* stage = Ginv + RP;         // (blockDim*RPT) * LD: staged rows (Grams)
+  double* Ginv = part + RP * RP;     // RP: 1 / G_jj (0 for skipped columns)
+  double* Hs = Ginv + RP;            // RP: G_{j-1,j} / G_jj (0 for skipped columns)
+  double* stage = Hs + RP;           // (blockDim*RPT) * LD: staged rows (Grams)
   double* Cs = stage + size_t(blockDim.x) * RPT * LD;  // (blockDim*RPT) * LD: rows of C
   double* aslots = Cs + size_t(blockDim.x) * RPT * LD;  // 2 x kMaxCluster: st.async sums
   uint64_t* abar = reinterpret_cast<uint64_t*>(aslots + 2 * kMaxCluster);  // 2 mbarriers
@@ -220,17 +242,25 @@ __global__ void __launch_bounds__(TPB) nnls_kernel(NnlsLaunch a) {
     Cs[lr * LD + l] = (lr < rpc && gr < a.rows && l < r) ? C[(long long)gr * r + l] : 0.0;
   }
   __syncthreads();
-  for (int j = threadIdx.x; j < RP; j += blockDim.x)
-    Ginv[j] = (j < r && Gs[j * RP + j] > 0.0) ? 1.0 / Gs[j * RP + j] : 0.0;
   double dmax = -INFINITY;
   for (int j = 0; j < r; ++j) dmax = fmax(dmax, Gs[j * RP + j]);
-  const double diag_floor = 1e-12 * dmax;
+  const double diag_floor = 1e-12 * dmax;  // nnls.cpp:16-19
+  // columns with G_jj <= floor are skipped: ginv = h = 0 leaves them as they are
+  unsigned long long okmask = 0;
+  for (int j = 0; j < r; ++j)
+    if (Gs[j * RP + j] > diag_floor) okmask |= 1ull << j;
+  for (int j = threadIdx.x; j < RP; j += blockDim.x) {
+    const bool ok = (okmask >> j) & 1;
+    const double gi = ok ? 1.0 / Gs[j * RP + j] : 0.0;
+    Ginv[j] = gi;
+    Hs[j] = (ok && j > 0) ? Gs[(j - 1) * RP + j] * gi : 0.0;
+  }
   if (threadIdx.x == 0) {
     for (int b = 0; b < 2; ++b)
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&abar[b])) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  cl.sync();  // every CTA's mbarriers exist before any st.async targets them
+  cl.sync();  // every CTA's mbarriers exist before any st.async targets them; Ginv/Hs visible
 
   double W[RPT][RP];
 #pragma unroll
@@ -243,7 +273,7 @@ __global__ void __launch_bounds__(TPB) nnls_kernel(NnlsLaunch a) {
   // updated in this pass (nnls.cpp:22). It is assembled as
   //   P[j] = sum_{l >= j} W_old[l] G[l][j]      (all j at once, ILP)
   //        + sum_{l < j}  W_new[l] G[l][j]      (added as columns finish),
-  // so the serial chain from column j-1 to j is one FMA, not a dot product.
+  // so column j needs no dot product once column j-1 is known.
   // The division by G_jj is a multiply by its reciprocal (<= 1 ulp apart).
   // RPT rows per thread share every G read and interleave their chains.
   double first = -1.0;
@@ -251,7 +281,7 @@ __global__ void __launch_bounds__(TPB) nnls_kernel(NnlsLaunch a) {
   long long prof_red = 0;  // diagnostics: cycles in the per-sweep cluster reduction
   const long long prof_t0 = clock64();
   constexpr bool kIncremental = RP <= 32;  // P[] costs RPT*RP more registers
-  for (; s < max_iters; ++s) {
+  auto sweep = [&]() -> double {
     double P[RPT][kIncremental ? RP : 1];
     if constexpr (kIncremental) {
       // row l of G is contiguous: 16-byte broadcast reads; P[j] still sums
@@ -274,17 +304,48 @@ __global__ void __launch_bounds__(TPB) nnls_kernel(NnlsLaunch a) {
       }
     }
     double d2 = 0.0;
+    if constexpr (kIncremental) {
+      // Branch-free: padded (j >= r) and skipped columns have ginv = h = 0 and
+      // come out unchanged. With P[j] holding every term of (W G)[row, j] but
+      // column j-1's,
+      //   numer_j / G_jj = (C_j - P[j]) / G_jj + W_j - h_j * Wnew_{j-1},
+      // whose first part is ready a column early: the serial chain from
+      // column j-1 to j is one FMA and the clip.
+      double prev[RPT];
 #pragma unroll
-    for (int j = 0; j < RP; ++j) {
-      if (j < r) {
-        const double gjj = Gs[j * RP + j];
-        const double ginv = Ginv[j];
+      for (int j = 0; j < RP; ++j) {
+        const double ginv = Ginv[j], h = Hs[j];
+        const bool ok = (okmask >> j) & 1ull;
 #pragma unroll
         for (int i = 0; i < RPT; ++i) {
-          double prod;
-          if constexpr (kIncremental) {
-            prod = P[i][j];
-          } else {
+          const double c = Cs[(int(threadIdx.x) + i * int(blockDim.x)) * LD + j];
+          const double t = fma(c - P[i][j], ginv, W[i][j]);
+          const double v = j == 0 ? t : fma(-h, prev[i], t);
+          const double nw = (ok && v < 0.0) ? 0.0 : v;  // cwiseMax(0.0)
+          const double d = nw - W[i][j];
+          d2 = fma(d, d, d2);
+          W[i][j] = nw;
+          prev[i] = nw;
+        }
+        // columns q >= j + 2 (column j + 1 takes this one through h)
+#pragma unroll
+        for (int q = (j + 2) & ~1; q < RP; q += 2) {
+          const double2 g = *reinterpret_cast<const double2*>(&Gs[j * RP + q]);
+#pragma unroll
+          for (int i = 0; i < RPT; ++i) {
+            if (q >= j + 2) P[i][q] = fma(W[i][j], g.x, P[i][q]);
+            P[i][q + 1] = fma(W[i][j], g.y, P[i][q + 1]);
+          }
+        }
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < RP; ++j) {
+        if (j < r) {
+          const double gjj = Gs[j * RP + j];
+          const double ginv = Ginv[j];
+#pragma unroll
+          for (int i = 0; i < RPT; ++i) {
             double p0 = 0.0, p1 = 0.0, p2 = 0.0, p3 = 0.0;
 #pragma unroll
             for (int l = 0; l < RP; l += 4) {
@@ -293,39 +354,61 @@ __global__ void __launch_bounds__(TPB) nnls_kernel(NnlsLaunch a) {
               p2 = fma(W[i][l + 2], Gs[(l + 2) * RP + j], p2);
               p3 = fma(W[i][l + 3], Gs[(l + 3) * RP + j], p3);
             }
-            prod = (p0 + p1) + (p2 + p3);
-          }
-          if (gjj > diag_floor) {
-            const double c = Cs[(int(threadIdx.x) + i * int(blockDim.x)) * LD + j];
-            const double numer = __dadd_rn(__dsub_rn(c, prod), __dmul_rn(gjj, W[i][j]));
-            const double nw = clip0(__dmul_rn(numer, ginv));
-            const double d = nw - W[i][j];
-            d2 = fma(d, d, d2);
-            W[i][j] = nw;
-          }
-        }
-        if constexpr (kIncremental) {
-#pragma unroll
-          for (int q = (j + 1) & ~1; q < RP; q += 2) {
-            const double2 g = *reinterpret_cast<const double2*>(&Gs[j * RP + q]);
-#pragma unroll
-            for (int i = 0; i < RPT; ++i) {
-              if (q > j) P[i][q] = fma(W[i][j], g.x, P[i][q]);
-              P[i][q + 1] = fma(W[i][j], g.y, P[i][q + 1]);
+            const double prod = (p0 + p1) + (p2 + p3);
+            if (gjj > diag_floor) {
+              const double c = Cs[(int(threadIdx.x) + i * int(blockDim.x)) * LD + j];
+              const double numer = __dadd_rn(__dsub_rn(c, prod), __dmul_rn(gjj, W[i][j]));
+              const double nw = clip0(__dmul_rn(numer, ginv));
+              const double d = nw - W[i][j];
+              d2 = fma(d, d, d2);
+              W[i][j] = nw;
             }
           }
         }
       }
     }
-    const long long tr0 = clock64();
-    // sweep s uses buffer s & 1 for the (s >> 1)-th time
-    const double change =
-        sqrt(cluster_sum_async(d2, red, aslots + (s & 1) * kMaxCluster, &abar[s & 1], uint32_t(s >> 1) & 1u, cl));
-    prof_red += clock64() - tr0;
-    if (s == 0) first = change;
-    if (change <= tol * first) {
+    return d2;
+  };
+  // Sweep s + 1 runs speculatively while the cluster reduction of sweep s's
+  // change is in flight; if sweep s meets the stop rule its result is
+  // restored from Wsave (nnls.cpp:33-39: the stop test follows the sweep).
+  constexpr bool kSpeculate = kIncremental;
+  auto post = [&](double d2, int k) {
+    return cluster_post(d2, red, aslots + (k & 1) * kMaxCluster, &abar[k & 1], cl);
+  };
+  auto fin = [&](double b, int k) {
+    return cluster_fin(b, aslots + (k & 1) * kMaxCluster, &abar[k & 1], uint32_t(k >> 1) & 1u, cl);
+  };
+  if (max_iters > 0) {
+    double b = post(sweep(), 0);
+    for (;;) {
+      const bool spec = kSpeculate && s + 1 < max_iters;
+      double Wsave[RPT][RP];
+      double d2n = 0.0;
+      if (spec) {
+#pragma unroll
+        for (int i = 0; i < RPT; ++i)
+#pragma unroll
+          for (int l = 0; l < RP; ++l) Wsave[i][l] = W[i][l];
+        d2n = sweep();
+      }
+      const long long tr0 = clock64();
+      const double ch2 = fin(b, s);  // ||W_{s+1} - W_s||_F^2
+      prof_red += clock64() - tr0;
+      if (s == 0) first = sqrt(ch2);
       ++s;
-      break;
+      if (stop_rule(ch2, tol * first)) {
+        if (spec) {
+#pragma unroll
+          for (int i = 0; i < RPT; ++i)
+#pragma unroll
+            for (int l = 0; l < RP; ++l) W[i][l] = Wsave[i][l];
+        }
+        break;
+      }
+      if (s >= max_iters) break;
+      if (!spec) d2n = sweep();
+      b = post(d2n, s);
     }
   }
 
@@ -456,7 +539,7 @@ void launch_rpt(const NnlsLaunch& a, cudaStream_t s) {
   if (threads > TPB) throw Unsupported("factor too tall for the fused NNLS kernel");
   const size_t nloc = size_t(threads) * RPT;
   const size_t smem =
-      sizeof(double) * (2 * RP * RP + 32 + 2 * kMaxCluster + RP + 2 * nloc * (RP + 1) + 2 * kMaxCluster + 2);
+      sizeof(double) * (2 * RP * RP + 32 + 2 * kMaxCluster + 2 * RP + 2 * nloc * (RP + 1) + 2 * kMaxCluster + 2);
   auto fn = nnls_kernel<RP, RPT, TPB>;
   NTF_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   if (cl > 8) NTF_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
@@ -477,17 +560,9 @@ void launch_rpt(const NnlsLaunch& a, cudaStream_t s) {
   NTF_CUDA(cudaLaunchKernelExC(&cfg, reinterpret_cast<const void*>(fn), params));
 }
 
-// Rows per thread: 1 by default (the sweep is latency-bound per warp);
-// NTF_NNLS_RPT=2 selects two interleaved rows where registers allow.
+// One row per thread (the sweep is latency-bound per warp).
 template <int RP, int TPB>
 void launch_rp(const NnlsLaunch& a, cudaStream_t s) {
-  static const int rpt = [] {
-    const char* e = std::getenv("NTF_NNLS_RPT");
-    return e ? std::atoi(e) : 1;
-  }();
-  if constexpr (RP <= 24) {
-    if (rpt == 2) return launch_rpt<RP, 2, TPB>(a, s);
-  }
   launch_rpt<RP, 1, TPB>(a, s);
 }
 
