@@ -31,10 +31,21 @@ namespace ntfb {
 namespace {
 
 constexpr int kMaxCluster = 16;
+constexpr int kMaxWarps = 8;  // per CTA (256 threads)
 
 // diagnostics: CTA 0's sweep-loop cycles, of which in the cluster reduction,
 // sweeps, calls (read with ntfb::nnls_prof_read)
-__device__ unsigned long long g_nnls_prof[4];
+__device__ unsigned long long g_nnls_prof[8];  // + [4] cycles in passes, [5] passes, [6] triangle cycles
+// per-pass probes (compile with -DNTF_NNLS_PROFILE=1): clock reads cost ~30 cycles each
+#ifndef NTF_NNLS_PROFILE
+#define NTF_NNLS_PROFILE 0
+#endif
+#ifndef NTF_NNLS_SYNCWARP
+#define NTF_NNLS_SYNCWARP 1
+#endif
+__device__ __forceinline__ long long pclock() { return NTF_NNLS_PROFILE ? clock64() : 0; }
+// globaltimer of post / fin completion of pass 4, per (CTA, warp), last call (profile builds)
+__device__ unsigned long long g_nnls_skew[3][128];
 
 __device__ __forceinline__ unsigned long long globaltimer() {
   unsigned long long t;
@@ -82,37 +93,36 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
-// Sum over the cluster without a cluster barrier, in two halves so a sweep
-// can run between them: cluster_post sends this CTA's block sum to slot [me]
+// Sum over the cluster without any barrier, in two halves so a sweep can
+// run between them. cluster_post: every warp reduces its lanes (butterfly,
+// same bits in every lane) and sends the value to slot [cta * nwarps + warp]
 // of every CTA with st.async, which completes transaction bytes on the
-// receiver's mbarrier `bar` (expecting n*8 bytes plus its own arrival);
-// cluster_fin waits for the n slots (`phase` = parity of this use of `bar`)
-// and adds them in CTA-rank order. The same bits reach every CTA. A slot
-// buffer is reused two reductions later: a CTA can only post there after
-// every CTA has posted the reduction in between, i.e. after reading it.
-__device__ double cluster_post(double v, double* red, double* slots, uint64_t* bar, cg::cluster_group& cl) {
-  const double b = block_sum(v, red);
-  const unsigned n = cl.num_blocks();
-  if (n == 1) return b;
-  const unsigned me = cl.block_rank();
+// receiver's mbarrier `bar` (expecting n * nwarps * 8 bytes plus one arrival,
+// by thread 0). cluster_fin waits for the slots (`phase` = parity of this use
+// of `bar`) and adds them in a fixed order. The same bits reach every thread.
+// A slot buffer is reused two reductions later: a warp can only post there
+// after every warp has posted the reduction in between, i.e. after reading.
+__device__ void cluster_post(double v, double* slots, uint64_t* bar, cg::cluster_group& cl) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const unsigned n = cl.num_blocks(), me = cl.block_rank();
+  const unsigned nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0)
     asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-                 "r"(n * 8u)
+                 "r"(n * nw * 8u)
                  : "memory");
-  if (threadIdx.x < n) {
+  if (lane < n) {
     uint32_t raddr, rbar;
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(raddr) : "r"(smem_u32(&slots[me])), "r"(threadIdx.x));
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rbar) : "r"(smem_u32(bar)), "r"(threadIdx.x));
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(raddr) : "r"(smem_u32(&slots[me * nw + warp])), "r"(lane));
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rbar) : "r"(smem_u32(bar)), "r"(lane));
     asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(raddr),
-                 "l"(__double_as_longlong(b)), "r"(rbar)
+                 "l"(__double_as_longlong(v)), "r"(rbar)
                  : "memory");
   }
-  return b;
 }
 
-__device__ double cluster_fin(double b, const double* slots, uint64_t* bar, uint32_t phase, cg::cluster_group& cl) {
-  const unsigned n = cl.num_blocks();
-  if (n == 1) return b;
+__device__ double cluster_fin(const double* slots, uint64_t* bar, uint32_t phase, cg::cluster_group& cl) {
+  const unsigned total = cl.num_blocks() * (blockDim.x >> 5);
   asm volatile(
       "{\n\t.reg .pred p;\n"
       "W_%=:\n\t"
@@ -122,10 +132,20 @@ __device__ double cluster_fin(double b, const double* slots, uint64_t* bar, uint
       : "memory");
   // (st.async data is visible once its complete_tx is observed; no
   // cluster-scope acquire, which would invalidate L1)
-  double s = 0.0;
-  for (unsigned k = 0; k < n; ++k) s += slots[k];
+  // lane l adds slots l, l + 32, ... (loads in flight together), then a
+  // butterfly: identical operations in every warp, so identical bits
+  const unsigned lane = threadIdx.x & 31;
+  double v = 0.0;
+#pragma unroll
+  for (int i = 0; i < kMaxCluster * kMaxWarps / 32; ++i) {
+    const unsigned e = lane + 32u * i;
+    const double x = e < total ? slots[e] : 0.0;
+    v = i == 0 ? x : v + x;
+  }
   __syncwarp();  // every lane has read the slots before any lane posts again
-  return s;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
 }
 
 // sqrt(ch2) <= thr (nnls.cpp:38) without the square root on the sweep
@@ -180,37 +200,51 @@ __device__ void cluster_gram(const double* stage, int nrows, double* part, int r
   cl.sync();  // partials are reused by the next Gram; dst visible cluster-wide
 }
 
-template <int RP, int RPT, int TPB>
-__global__ void __launch_bounds__(TPB) nnls_kernel(NnlsLaunch a) {
+// Lanes per row Q (see the sweep below).
+template <int RP, int Q>
+struct SweepShape {
+  static constexpr bool kIncremental = RP <= 32;  // per-column partial sums in registers
+  static constexpr int PQ = RP / Q;               // columns per lane
+  static constexpr int PQP = (PQ + 1) & ~1;        // padded: 16-byte aligned per-lane runs
+  static constexpr int RS = Q * PQP;               // row stride of the lane-permuted matrices
+  static_assert(RP % Q == 0 && (Q == 1 || kIncremental), "lane split needs the incremental sweep");
+};
+
+template <int RP, int Q, int TPB>
+__global__ void __launch_bounds__(TPB, 1) nnls_kernel(NnlsLaunch a) {
+  using Shape = SweepShape<RP, Q>;
   constexpr int LD = RP + 1;
+  constexpr int PQ = Shape::PQ, PQP = Shape::PQP, RS = Shape::RS;
+  constexpr bool kIncremental = Shape::kIncremental;
   extern __shared__ double smem[];
-  double* Gs = smem;                 // RP*RP
-  double* red = Gs + RP * RP;        // 32
-  double* pub = red + 32;            // 2 x kMaxCluster: pushed block sums (by parity)
+  const int nloc = int(blockDim.x) / Q;  // row slots per CTA
+  double* Gs = smem;                     // RP*RP
+  double* red = Gs + RP * RP;            // 32
+  double* pub = red + 32;                // 2 x kMaxCluster: pushed block sums (by parity)
   double* part = pub + 2 * kMaxCluster;  // RP*RP: Gram partial of this CTA
-  double* Ginv = part + RP * RP;     // RP: 1 / G_jj (0 for skipped columns)
-  double* Hs = Ginv + RP;            // RP: G_{j-1,j} / G_jj (0 for skipped columns)
-  double* stage = Hs + RP;           // (blockDim*RPT) * LD: staged rows (Grams)
-  double* Cs = stage + size_t(blockDim.x) * RPT * LD;  // (blockDim*RPT) * LD: rows of C
-  double* aslots = Cs + size_t(blockDim.x) * RPT * LD;  // 2 x kMaxCluster: st.async sums
-  uint64_t* abar = reinterpret_cast<uint64_t*>(aslots + 2 * kMaxCluster);  // 2 mbarriers
+  double* Ginv = part + RP * RP;         // RP: 1 / G_jj (0 for skipped columns)
+  // column constants (hd_j, lo_j) = (G[j-1][j] / G_jj, clip bound 0), (0, -inf) when skipped
+  double* HL = Ginv + RP;                // 2*RP
+  // lane-permuted [l][k][m] (column q = m Q + k, lane k's run contiguous):
+  double* HmP = HL + 2 * RP;             // RP*RS: G[l][q] / G_qq for l + 2 <= q (pushes), else 0
+  double* GtP = HmP + (kIncremental ? RP * RS : 0);  // RP*RS: G[l][q] / G_qq for l > q, -1 at l == q if skipped
+  double* stage = GtP + (kIncremental ? RP * RS : 0);  // nloc * LD: staged rows (Grams)
+  double* Cs = stage + size_t(nloc) * LD;  // nloc * LD: rows of C
+  double* aslots = Cs + size_t(nloc) * LD;  // 2 x kMaxCluster*kMaxWarps: st.async sums
+  uint64_t* abar = reinterpret_cast<uint64_t*>(aslots + 2 * kMaxCluster * kMaxWarps);  // 2 mbarriers
   cg::cluster_group cl = cg::this_cluster();
 
   RunState* st = a.st;
   if (st && st->done) return;  // budget exhausted: the whole iteration is a no-op (uniform)
 
   const int r = a.rank, mode = a.mode;
-  const int nloc = int(blockDim.x) * RPT;                              // row slots per CTA
-  const int rpc = (a.rows + int(gridDim.x) - 1) / int(gridDim.x);    // rows per CTA
-  // thread t owns local rows t, t + blockDim, ... (coalesced loads/stores)
-  int row[RPT];
-  bool valid[RPT];
-#pragma unroll
-  for (int i = 0; i < RPT; ++i) {
-    const int lr = int(threadIdx.x) + i * int(blockDim.x);
-    row[i] = int(blockIdx.x) * rpc + lr;
-    valid[i] = lr < rpc && row[i] < a.rows;
-  }
+  const int rpc = (a.rows + int(gridDim.x) - 1) / int(gridDim.x);  // rows per CTA
+  // Q consecutive lanes own one row: lane k of the group keeps the sweep
+  // products of columns k, k + Q, ...; W is replicated in the group.
+  const int lr = int(threadIdx.x) / Q, k = int(threadIdx.x) % Q;
+  const int row = int(blockIdx.x) * rpc + lr;
+  const bool valid = lr < rpc && row < a.rows;
+  const bool lead = valid && k == 0;  // writes the row
   DevFactors* F = a.F;
   const int sel = F ? F->sel[mode] : 0;
   double* X = F ? F->x[mode][sel] : nullptr;
@@ -235,11 +269,11 @@ __global__ void __launch_bounds__(TPB) nnls_kernel(NnlsLaunch a) {
     }
     Gs[e] = g;
   }
-  // rows of C in shared memory (read once per column per sweep, off the chain)
+  // rows of C in shared memory
   for (int e = threadIdx.x; e < nloc * RP; e += blockDim.x) {
-    const int lr = e / RP, l = e % RP;
-    const int gr = int(blockIdx.x) * rpc + lr;
-    Cs[lr * LD + l] = (lr < rpc && gr < a.rows && l < r) ? C[(long long)gr * r + l] : 0.0;
+    const int i = e / RP, l = e % RP;
+    const int gr = int(blockIdx.x) * rpc + i;
+    Cs[i * LD + l] = (i < rpc && gr < a.rows && l < r) ? C[(long long)gr * r + l] : 0.0;
   }
   __syncthreads();
   double dmax = -INFINITY;
@@ -253,163 +287,207 @@ __global__ void __launch_bounds__(TPB) nnls_kernel(NnlsLaunch a) {
     const bool ok = (okmask >> j) & 1;
     const double gi = ok ? 1.0 / Gs[j * RP + j] : 0.0;
     Ginv[j] = gi;
-    Hs[j] = (ok && j > 0) ? Gs[(j - 1) * RP + j] * gi : 0.0;
+    HL[2 * j] = j > 0 ? Gs[(j - 1) * RP + j] * gi : 0.0;
+    HL[2 * j + 1] = ok ? 0.0 : -INFINITY;
+  }
+  for (int e = threadIdx.x; kIncremental && e < RP * RS; e += blockDim.x) {
+    const int l = e / RS, kk = (e % RS) / PQP, m = e % PQP, q = m * Q + kk;
+    double h = 0.0, g = 0.0;
+    if (m < PQ) {
+      const bool ok = (okmask >> q) & 1;
+      const double gi = ok ? 1.0 / Gs[q * RP + q] : 0.0;
+      h = l + 2 <= q ? Gs[l * RP + q] * gi : 0.0;
+      g = l > q ? Gs[l * RP + q] * gi : (l == q && !ok ? -1.0 : 0.0);
+    }
+    HmP[e] = h;
+    GtP[e] = g;
   }
   if (threadIdx.x == 0) {
     for (int b = 0; b < 2; ++b)
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&abar[b])) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  cl.sync();  // every CTA's mbarriers exist before any st.async targets them; Ginv/Hs visible
+  cl.sync();  // every CTA's mbarriers exist before any st.async targets them; Ginv/Hm/Gm visible
 
-  double W[RPT][RP];
+  double W[RP], WB[RP];  // the sweeps alternate W -> WB -> W ...
 #pragma unroll
-  for (int i = 0; i < RPT; ++i)
+  for (int l = 0; l < RP; ++l) W[l] = (valid && l < r) ? w0[(long long)row * r + l] : 0.0;
+  double cs[kIncremental ? PQ : 1];  // C / G_qq of this lane's columns q = m Q + k
 #pragma unroll
-    for (int l = 0; l < RP; ++l) W[i][l] = (valid[i] && l < r) ? w0[(long long)row[i] * r + l] : 0.0;
+  for (int m = 0; m < (kIncremental ? PQ : 1); ++m) cs[m] = Cs[lr * LD + m * Q + k] * Ginv[m * Q + k];
+  const int gbase = (int(threadIdx.x) & 31) & ~(Q - 1);  // first lane of the group
 
-  // ---- AHALS sweeps.
-  // Column j of a pass needs prod_j = (W G)[row, j] with columns < j already
-  // updated in this pass (nnls.cpp:22). It is assembled as
-  //   P[j] = sum_{l >= j} W_old[l] G[l][j]      (all j at once, ILP)
-  //        + sum_{l < j}  W_new[l] G[l][j]      (added as columns finish),
-  // so column j needs no dot product once column j-1 is known.
-  // The division by G_jj is a multiply by its reciprocal (<= 1 ulp apart).
-  // RPT rows per thread share every G read and interleave their chains.
+  // ---- AHALS sweeps (nnls.cpp:15-49).
+  // Column j of a pass is (Gauss-Seidel, nnls.cpp:22)
+  //   numer_j / G_jj = t_j - sum_{l < j} G[l][j] / G_jj W_new[l],
+  //   t_j = C_j / G_jj - sum_{l > j} G[l][j] / G_jj W_old[l]
+  // (the reference's "minus W G_j plus G_jj W_j", the l = j terms cancelled).
+  // Lane k of a row's group owns the pending sums u of columns k, k + Q, ...:
+  // it forms their t (the triangle) at the start of the pass and pushes every
+  // new W[l] into them, except into column l + 1. Column j's owner hands u_j
+  // to the group two columns early (shuffle); every lane adds the last term
+  // -hd_j W_new[j-1] itself and clips, so the serial chain per column is one
+  // FMA and the clip, and the shuffle has a column of slack. Division by G_jj
+  // is a multiply by its reciprocal (<= 1 ulp apart). Padded (j >= r) and
+  // skipped columns have t_j = W_j (GtP diagonal -1), no terms, no clip.
+  // __syncwarp() between columns keeps ptxas from sinking work into long
+  // per-column chains (in-order issue would serialise them); every operand
+  // of column j + 1 is loaded during column j. A pass reads Wi, writes Wo.
   double first = -1.0;
   int s = 0;
   long long prof_red = 0;  // diagnostics: cycles in the per-sweep cluster reduction
   const long long prof_t0 = clock64();
-  constexpr bool kIncremental = RP <= 32;  // P[] costs RPT*RP more registers
-  auto sweep = [&]() -> double {
-    double P[RPT][kIncremental ? RP : 1];
-    if constexpr (kIncremental) {
-      // row l of G is contiguous: 16-byte broadcast reads; P[j] still sums
-      // l = j, j+1, ... in ascending order
-#pragma unroll
-      for (int i = 0; i < RPT; ++i)
-#pragma unroll
-        for (int j = 0; j < RP; ++j) P[i][j] = 0.0;
-#pragma unroll
-      for (int l = 0; l < RP; ++l) {
-#pragma unroll
-        for (int j = 0; j <= l; j += 2) {
-          const double2 g = *reinterpret_cast<const double2*>(&Gs[l * RP + j]);
-#pragma unroll
-          for (int i = 0; i < RPT; ++i) {
-            P[i][j] = fma(W[i][l], g.x, P[i][j]);
-            if (j + 1 <= l) P[i][j + 1] = fma(W[i][l], g.y, P[i][j + 1]);
-          }
-        }
-      }
-    }
+  long long prof_pass = 0, prof_tri = 0, prof_np = 0;
+  auto sweep = [&](const double(&Wi)[RP], double(&Wo)[RP]) -> double {
+    const long long ps0 = pclock();
     double d2 = 0.0;
     if constexpr (kIncremental) {
-      // Branch-free: padded (j >= r) and skipped columns have ginv = h = 0 and
-      // come out unchanged. With P[j] holding every term of (W G)[row, j] but
-      // column j-1's,
-      //   numer_j / G_jj = (C_j - P[j]) / G_jj + W_j - h_j * Wnew_{j-1},
-      // whose first part is ready a column early: the serial chain from
-      // column j-1 to j is one FMA and the clip.
-      double prev[RPT];
+      const double* gt = GtP + k * PQP;
+      const double* hm = HmP + k * PQP;
+      double u[PQP], ub[PQP];  // two accumulators per slot (even / odd l): half the chain
 #pragma unroll
-      for (int j = 0; j < RP; ++j) {
-        const double ginv = Ginv[j], h = Hs[j];
-        const bool ok = (okmask >> j) & 1ull;
+      for (int m = 0; m < PQP; ++m) u[m] = ub[m] = 0.0;
 #pragma unroll
-        for (int i = 0; i < RPT; ++i) {
-          const double c = Cs[(int(threadIdx.x) + i * int(blockDim.x)) * LD + j];
-          const double t = fma(c - P[i][j], ginv, W[i][j]);
-          const double v = j == 0 ? t : fma(-h, prev[i], t);
-          const double nw = (ok && v < 0.0) ? 0.0 : v;  // cwiseMax(0.0)
-          const double d = nw - W[i][j];
-          d2 = fma(d, d, d2);
-          W[i][j] = nw;
-          prev[i] = nw;
-        }
-        // columns q >= j + 2 (column j + 1 takes this one through h)
+      for (int l = 0; l < RP; ++l) {
+        const int mmax = (l / Q < PQ - 1) ? l / Q : PQ - 1;  // slots with a column <= l
+        double* acc = (l & 1) ? ub : u;
 #pragma unroll
-        for (int q = (j + 2) & ~1; q < RP; q += 2) {
-          const double2 g = *reinterpret_cast<const double2*>(&Gs[j * RP + q]);
-#pragma unroll
-          for (int i = 0; i < RPT; ++i) {
-            if (q >= j + 2) P[i][q] = fma(W[i][j], g.x, P[i][q]);
-            P[i][q + 1] = fma(W[i][j], g.y, P[i][q + 1]);
-          }
+        for (int m = 0; m <= mmax; m += 2) {
+          const double2 g = *reinterpret_cast<const double2*>(gt + l * RS + m);
+          acc[m] = fma(Wi[l], g.x, acc[m]);
+          if (m + 1 <= mmax) acc[m + 1] = fma(Wi[l], g.y, acc[m + 1]);
         }
       }
+#pragma unroll
+      for (int m = 0; m < PQ; ++m) u[m] = cs[m] - (u[m] + ub[m]);
+      prof_tri += pclock() - ps0;
+      auto bcast = [&](int j) {  // u_j from its owner
+        if constexpr (Q > 1)
+          return __shfl_sync(0xffffffffu, u[j / Q], gbase | (j % Q));
+        else
+          return u[j];
+      };
+      // operands of the pushes of column j (hm row j, slots m >= (j + 2) / Q)
+      // and of its chain step (hd_j, lo_j), loaded two columns ahead (shared
+      // loads take ~50 cycles; ptxas issues them no earlier than written)
+      double hp[3][PQP];
+      double2 hl[3];
+      auto load_ops = [&](int j) {
+        const int m0 = ((j + 2) / Q) & ~1;
+#pragma unroll
+        for (int m = m0; m < PQ; m += 2) {
+          const double2 h = *reinterpret_cast<const double2*>(hm + j * RS + m);
+          hp[j % 3][m] = h.x;
+          hp[j % 3][m + 1] = h.y;
+        }
+        hl[j % 3] = *reinterpret_cast<const double2*>(HL + 2 * j);
+      };
+      double pend[RP];  // u_j as handed over (all terms but column j-1's)
+      pend[0] = bcast(0);
+      if (RP > 1) pend[1] = bcast(1);
+      load_ops(0);
+      if (RP > 1) load_ops(1);
+      double d2b = 0.0;
+#pragma unroll
+      for (int j = 0; j < RP; ++j) {
+        if (j + 2 < RP) load_ops(j + 2);
+        const double v = j == 0 ? pend[0] : fma(-hl[j % 3].x, Wo[j - 1], pend[j]);
+        const double nw = v < hl[j % 3].y ? 0.0 : v;  // cwiseMax(0.0)
+        const double dd = nw - Wi[j];
+        if (j & 1)
+          d2b = fma(dd, dd, d2b);
+        else
+          d2 = fma(dd, dd, d2);
+        Wo[j] = nw;
+#pragma unroll
+        for (int m = (j + 2) / Q; m < PQ; ++m) u[m] = fma(-nw, hp[j % 3][m], u[m]);
+        if (j + 2 < RP) pend[j + 2] = bcast(j + 2);
+        if (NTF_NNLS_SYNCWARP) __syncwarp();
+      }
+      d2 += d2b;
     } else {
+#pragma unroll
+      for (int j = 0; j < RP; ++j) Wo[j] = Wi[j];
 #pragma unroll
       for (int j = 0; j < RP; ++j) {
         if (j < r) {
           const double gjj = Gs[j * RP + j];
           const double ginv = Ginv[j];
+          double p0 = 0.0, p1 = 0.0, p2 = 0.0, p3 = 0.0;
 #pragma unroll
-          for (int i = 0; i < RPT; ++i) {
-            double p0 = 0.0, p1 = 0.0, p2 = 0.0, p3 = 0.0;
-#pragma unroll
-            for (int l = 0; l < RP; l += 4) {
-              p0 = fma(W[i][l + 0], Gs[(l + 0) * RP + j], p0);
-              p1 = fma(W[i][l + 1], Gs[(l + 1) * RP + j], p1);
-              p2 = fma(W[i][l + 2], Gs[(l + 2) * RP + j], p2);
-              p3 = fma(W[i][l + 3], Gs[(l + 3) * RP + j], p3);
-            }
-            const double prod = (p0 + p1) + (p2 + p3);
-            if (gjj > diag_floor) {
-              const double c = Cs[(int(threadIdx.x) + i * int(blockDim.x)) * LD + j];
-              const double numer = __dadd_rn(__dsub_rn(c, prod), __dmul_rn(gjj, W[i][j]));
-              const double nw = clip0(__dmul_rn(numer, ginv));
-              const double d = nw - W[i][j];
-              d2 = fma(d, d, d2);
-              W[i][j] = nw;
-            }
+          for (int l = 0; l < RP; l += 4) {
+            p0 = fma(Wo[l + 0], Gs[(l + 0) * RP + j], p0);
+            p1 = fma(Wo[l + 1], Gs[(l + 1) * RP + j], p1);
+            p2 = fma(Wo[l + 2], Gs[(l + 2) * RP + j], p2);
+            p3 = fma(Wo[l + 3], Gs[(l + 3) * RP + j], p3);
+          }
+          const double prod = (p0 + p1) + (p2 + p3);
+          if (gjj > diag_floor) {
+            const double c = Cs[lr * LD + j];
+            const double numer = __dadd_rn(__dsub_rn(c, prod), __dmul_rn(gjj, Wo[j]));
+            const double nw = clip0(__dmul_rn(numer, ginv));
+            const double dd = nw - Wo[j];
+            d2 = fma(dd, dd, d2);
+            Wo[j] = nw;
           }
         }
       }
     }
-    return d2;
+    prof_pass += pclock() - ps0;
+    ++prof_np;
+    return k == 0 ? d2 : 0.0;  // each row counted once
   };
+
   // Sweep s + 1 runs speculatively while the cluster reduction of sweep s's
-  // change is in flight; if sweep s meets the stop rule its result is
-  // restored from Wsave (nnls.cpp:33-39: the stop test follows the sweep).
+  // change is in flight; if sweep s meets the stop rule, its result (the
+  // other buffer) is kept (nnls.cpp:33-39: the stop test follows the sweep).
   constexpr bool kSpeculate = kIncremental;
-  auto post = [&](double d2, int k) {
-    return cluster_post(d2, red, aslots + (k & 1) * kMaxCluster, &abar[k & 1], cl);
+  auto post = [&](double d2, int j) {
+    if (NTF_NNLS_PROFILE && j == 4 && (threadIdx.x & 31) == 0)
+      g_nnls_skew[0][cl.block_rank() * (blockDim.x >> 5) + (threadIdx.x >> 5)] = globaltimer();
+    cluster_post(d2, aslots + (j & 1) * kMaxCluster * kMaxWarps, &abar[j & 1], cl);
   };
-  auto fin = [&](double b, int k) {
-    return cluster_fin(b, aslots + (k & 1) * kMaxCluster, &abar[k & 1], uint32_t(k >> 1) & 1u, cl);
+  auto fin = [&](int j) {
+    return cluster_fin(aslots + (j & 1) * kMaxCluster * kMaxWarps, &abar[j & 1], uint32_t(j >> 1) & 1u, cl);
   };
+  bool inB = false;  // result in WB
   if (max_iters > 0) {
-    double b = post(sweep(), 0);
-    for (;;) {
+    post(sweep(W, WB), 0);
+    bool done = false;
+    // current result in Wc (posted); the next pass goes to Wn
+    auto step = [&](double(&Wc)[RP], double(&Wn)[RP]) {
       const bool spec = kSpeculate && s + 1 < max_iters;
-      double Wsave[RPT][RP];
       double d2n = 0.0;
-      if (spec) {
-#pragma unroll
-        for (int i = 0; i < RPT; ++i)
-#pragma unroll
-          for (int l = 0; l < RP; ++l) Wsave[i][l] = W[i][l];
-        d2n = sweep();
-      }
-      const long long tr0 = clock64();
-      const double ch2 = fin(b, s);  // ||W_{s+1} - W_s||_F^2
-      prof_red += clock64() - tr0;
+      if (spec) d2n = sweep(Wc, Wn);
+      const long long tr0 = pclock();
+      if (NTF_NNLS_PROFILE && s == 4 && (threadIdx.x & 31) == 0)
+        g_nnls_skew[2][cl.block_rank() * (blockDim.x >> 5) + (threadIdx.x >> 5)] = globaltimer();
+      const double ch2 = fin(s);  // ||W_{s+1} - W_s||_F^2
+      prof_red += pclock() - tr0;
+      if (NTF_NNLS_PROFILE && s == 4 && (threadIdx.x & 31) == 0)
+        g_nnls_skew[1][cl.block_rank() * (blockDim.x >> 5) + (threadIdx.x >> 5)] = globaltimer();
       if (s == 0) first = sqrt(ch2);
       ++s;
-      if (stop_rule(ch2, tol * first)) {
-        if (spec) {
-#pragma unroll
-          for (int i = 0; i < RPT; ++i)
-#pragma unroll
-            for (int l = 0; l < RP; ++l) W[i][l] = Wsave[i][l];
-        }
+      if (s >= max_iters || stop_rule(ch2, tol * first)) {
+        done = true;
+        return;
+      }
+      if constexpr (!kSpeculate) d2n = sweep(Wc, Wn);
+      post(d2n, s);
+    };
+    for (;;) {
+      step(WB, W);
+      if (done) {
+        inB = true;
         break;
       }
-      if (s >= max_iters) break;
-      if (!spec) d2n = sweep();
-      b = post(d2n, s);
+      step(W, WB);
+      if (done) break;
     }
+  }
+  if (inB) {
+#pragma unroll
+    for (int l = 0; l < RP; ++l) W[l] = WB[l];
   }
 
   if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -417,25 +495,25 @@ __global__ void __launch_bounds__(TPB) nnls_kernel(NnlsLaunch a) {
     g_nnls_prof[1] += prof_red;
     g_nnls_prof[2] += s;
     g_nnls_prof[3] += 1;
+    g_nnls_prof[4] += prof_pass;
+    g_nnls_prof[5] += prof_np;
+    g_nnls_prof[6] += prof_tri;
   }
   if (a.role == 2) {
+    if (lead) {
 #pragma unroll
-    for (int i = 0; i < RPT; ++i)
-      if (valid[i]) {
-#pragma unroll
-        for (int l = 0; l < RP; ++l)
-          if (l < r) a.w_out[(long long)row[i] * r + l] = W[i][l];
-      }
+      for (int l = 0; l < RP; ++l)
+        if (l < r) a.w_out[(long long)row * r + l] = W[l];
+    }
     if (blockIdx.x == 0 && threadIdx.x == 0 && a.sweeps_out) *a.sweeps_out = s;
     return;
   }
 
   // ---- Gram(W): needed by F-hat / f and, on a restart, as the new Gram.
+  if (k == 0) {
 #pragma unroll
-  for (int i = 0; i < RPT; ++i)
-#pragma unroll
-    for (int l = 0; l < RP; ++l)
-      stage[(int(threadIdx.x) + i * int(blockDim.x)) * LD + l] = (valid[i] && l < r) ? W[i][l] : 0.0;
+    for (int l = 0; l < RP; ++l) stage[lr * LD + l] = (valid && l < r) ? W[l] : 0.0;
+  }
   __syncthreads();
   double* gW = (a.role == 0) ? F->gram[mode][sel ^ 1] : F->gram[mode][sel];
   cluster_gram<RP>(stage, nloc, part, r, gW, cl);
@@ -445,25 +523,24 @@ __global__ void __launch_bounds__(TPB) nnls_kernel(NnlsLaunch a) {
   double* S = F->x[mode][sel ^ 1];
   float* X32 = F->x32[mode][sel];
   float* S32 = F->x32[mode][sel ^ 1];
-#pragma unroll
-  for (int i = 0; i < RPT; ++i) {
+  if (k == 0) {
 #pragma unroll
     for (int l = 0; l < RP; ++l) {
       double h = 0.0;
-      if (valid[i] && l < r) {
-        const long long o = (long long)row[i] * r + l;
+      if (valid && l < r) {
+        const long long o = (long long)row * r + l;
         if (a.role == 0) {
           const double old = X[o];
-          h = clip0(__dadd_rn(W[i][l], __dmul_rn(beta, __dsub_rn(W[i][l], old))));
-          S[o] = W[i][l];
-          if (S32) S32[o] = float(W[i][l]);
+          h = clip0(__dadd_rn(W[l], __dmul_rn(beta, __dsub_rn(W[l], old))));  // her.cpp:16-19
+          S[o] = W[l];
+          if (S32) S32[o] = float(W[l]);
         } else {
-          h = W[i][l];
+          h = W[l];
         }
         X[o] = h;
         if (X32) X32[o] = float(h);
       }
-      if (a.role == 0) stage[(int(threadIdx.x) + i * int(blockDim.x)) * LD + l] = h;
+      if (a.role == 0) stage[lr * LD + l] = h;
     }
   }
   if (a.role == 0) {
@@ -477,13 +554,11 @@ __global__ void __launch_bounds__(TPB) nnls_kernel(NnlsLaunch a) {
 
   // ---- objective at the (mixed) point: <W, C> and <W^T W, G>.
   double cross = 0.0;
+  if (lead) {
 #pragma unroll
-  for (int i = 0; i < RPT; ++i)
-    if (valid[i]) {
-#pragma unroll
-      for (int l = 0; l < RP; ++l)
-        if (l < r) cross += W[i][l] * Cs[(int(threadIdx.x) + i * int(blockDim.x)) * LD + l];
-    }
+    for (int l = 0; l < RP; ++l)
+      if (l < r) cross += W[l] * Cs[lr * LD + l];
+  }
   cross = cluster_sum(cross, red, pub, (s + 1) & 1, cl);
   if (blockIdx.x != 0 || threadIdx.x != 0) return;
 
@@ -493,7 +568,7 @@ __global__ void __launch_bounds__(TPB) nnls_kernel(NnlsLaunch a) {
   const double f = 0.5 * st->nsq - cross + 0.5 * quad;
 
   st->last_sweeps[mode] = s;
-  const int k = st->k + 1;
+  const int kk = st->k + 1;
   const double time_s = double(globaltimer() - st->t_start_ns) * 1e-9;
   TraceEntry rec;
   rec.f = f;
@@ -518,29 +593,28 @@ __global__ void __launch_bounds__(TPB) nnls_kernel(NnlsLaunch a) {
     rec.beta = 0.0;
     rec.restarted = 0;
   }
-  a.trace[k - 1] = rec;
+  a.trace[kk - 1] = rec;
   st->f_last = f;
-  st->k = k;
-  if ((st->max_iters > 0 && k >= st->max_iters) || (st->max_time_s > 0.0 && time_s >= st->max_time_s))
+  st->k = kk;
+  if ((st->max_iters > 0 && kk >= st->max_iters) || (st->max_time_s > 0.0 && time_s >= st->max_time_s))
     st->done = 1;
 }
 
-// Cluster size: one warp of RPT-row threads per CTA when the factor allows,
-// at most 16 CTAs (non-portable cluster size, B200 allows it).
-int cluster_size(int rows, int rows_per_warp) {
-  return std::max(1, std::min((rows + rows_per_warp - 1) / rows_per_warp, kMaxCluster));
-}
-
-template <int RP, int RPT, int TPB>
-void launch_rpt(const NnlsLaunch& a, cudaStream_t s) {
-  const int cl = cluster_size(a.rows, 32 * RPT);
+// Launch shape: Q lanes per row, about four warps per CTA (one per SM
+// sub-partition), at most 16 CTAs (non-portable cluster size, allowed on
+// B200); taller factors put more warps in each CTA.
+template <int RP, int Q, int TPB>
+bool launch_q(const NnlsLaunch& a, cudaStream_t s) {
+  const long long lanes = (long long)a.rows * Q;
+  const int cl = int(std::max(1LL, std::min<long long>((lanes + 127) / 128, kMaxCluster)));
   const int rpc = (a.rows + cl - 1) / cl;
-  const int threads = ((rpc + RPT - 1) / RPT + 31) / 32 * 32;
-  if (threads > TPB) throw Unsupported("factor too tall for the fused NNLS kernel");
-  const size_t nloc = size_t(threads) * RPT;
-  const size_t smem =
-      sizeof(double) * (2 * RP * RP + 32 + 2 * kMaxCluster + 2 * RP + 2 * nloc * (RP + 1) + 2 * kMaxCluster + 2);
-  auto fn = nnls_kernel<RP, RPT, TPB>;
+  const int threads = (rpc * Q + 31) / 32 * 32;
+  if (threads > TPB) return false;
+  const size_t nloc = size_t(threads) / Q;
+  using Shape = SweepShape<RP, Q>;
+  const size_t smem = sizeof(double) * (2 * RP * RP + (Shape::kIncremental ? 2 * RP * Shape::RS : 0) + 32 +
+                                        2 * kMaxCluster + 3 * RP + 2 * nloc * (RP + 1) + 2 * kMaxCluster * kMaxWarps + 2);
+  auto fn = nnls_kernel<RP, Q, TPB>;
   NTF_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   if (cl > 8) NTF_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   NnlsLaunch args = a;
@@ -558,20 +632,32 @@ void launch_rpt(const NnlsLaunch& a, cudaStream_t s) {
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   NTF_CUDA(cudaLaunchKernelExC(&cfg, reinterpret_cast<const void*>(fn), params));
+  return true;
 }
 
-// One row per thread (the sweep is latency-bound per warp).
+// Preferred lane split by padded rank, falling back to one lane per row for
+// factors too tall for it. NTF_NNLS_Q=1 forces one lane per row.
 template <int RP, int TPB>
 void launch_rp(const NnlsLaunch& a, cudaStream_t s) {
-  launch_rpt<RP, 1, TPB>(a, s);
+  static const int qenv = [] {
+    const char* e = std::getenv("NTF_NNLS_Q");
+    return e ? std::atoi(e) : 0;
+  }();
+  if constexpr (RP >= 12 && RP <= 32) {
+    if (qenv != 1 && launch_q<RP, 4, TPB>(a, s)) return;
+  } else if constexpr (RP == 8) {
+    if (qenv != 1 && launch_q<RP, 2, TPB>(a, s)) return;
+  }
+  if (!launch_q<RP, 1, TPB>(a, s)) throw Unsupported("factor too tall for the fused NNLS kernel");
 }
 
 }  // namespace
 
-void nnls_prof_read(unsigned long long out[4], bool reset) {
-  NTF_CUDA(cudaMemcpyFromSymbol(out, g_nnls_prof, sizeof(unsigned long long) * 4));
+void nnls_prof_read(unsigned long long out[8 + 384], bool reset) {
+  NTF_CUDA(cudaMemcpyFromSymbol(out, g_nnls_prof, sizeof(unsigned long long) * 8));
+  NTF_CUDA(cudaMemcpyFromSymbol(out + 8, g_nnls_skew, sizeof(unsigned long long) * 384));
   if (reset) {
-    const unsigned long long z[4] = {0, 0, 0, 0};
+    const unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     NTF_CUDA(cudaMemcpyToSymbol(g_nnls_prof, z, sizeof z));
   }
 }

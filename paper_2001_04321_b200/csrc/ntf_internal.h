@@ -123,7 +123,7 @@ struct NnlsLaunch {
 };
 void launch_nnls(const NnlsLaunch& a, cudaStream_t s);
 // diagnostics: {sweep-loop cycles, reduction cycles, sweeps, calls} of CTA 0
-void nnls_prof_read(unsigned long long out[4], bool reset);
+void nnls_prof_read(unsigned long long out[8 + 384], bool reset);
 
 int device_sm_count();
 

@@ -32,8 +32,16 @@ print(f"  inner sweeps/iteration: mean {np.mean(sw):.1f} max {max(sw)} over {len
       f"final f {tr.final_f():.3e}")
 import ctypes as _C
 from paper_2001_04321_b200 import _lib as _L
-_buf = (_C.c_ulonglong * 4)()
+_buf = (_C.c_ulonglong * (8 + 384))()
 if _L.lib().ntf_debug_nnls_prof(_buf, 1) == 0 and _buf[3]:
-    loop, red, sw, calls = list(_buf)
+    loop, red, sw, calls, pc, npass, tri, _ = list(_buf)[:8]
+    b = list(_buf)
+    post, fin, fs = b[8:136], b[136:264], b[264:392]
+    idx = [i for i in range(128) if post[i]]
+    if idx:
+        p0 = min(post[i] for i in idx)
+        print("  pass-4 per warp (ns from first post): post / fin start / fin end")
+        print("   " + " ".join(f"{post[i]-p0}/{fs[i]-p0}/{fin[i]-p0}" for i in idx[:24]))
     print(f"  nnls CTA0: {loop / calls:.0f} cyc/call, {sw / calls:.1f} sweeps/call, "
-          f"{loop / max(sw, 1):.0f} cyc/sweep of which reduction {red / max(sw, 1):.0f}")
+          f"{loop / max(sw, 1):.0f} cyc/sweep of which reduction {red / max(sw, 1):.0f}; "
+          f"pass {pc / max(npass, 1):.0f} cyc (triangle {tri / max(npass, 1):.0f}), {npass / calls:.1f} passes/call")
