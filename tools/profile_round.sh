@@ -1,0 +1,16 @@
+#!/bin/bash
+# Round profile capture (run under gpurun from the repo root):
+#   bench line, reference arm, launch list, full ncu capture of the top kernels.
+set -u
+R=${1:-r01}
+O=gpurun_out
+python bench.py > $O/bench_$R.json 2> $O/bench_$R.err; echo "bench rc=$?"
+python bench.py --impl reference --steps 3 --warmup 1 > $O/bench_ref_$R.json 2> $O/bench_ref_$R.err; echo "ref rc=$?"
+CMD="python bench.py --steps 5 --warmup 3 --no-cpu-baseline"
+$CMD > $O/plain_$R.log 2>&1 && \
+  ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_$R.csv $CMD > $O/ncu_launch_$R.log 2>&1
+echo "launch list rc=$?"
+$CMD > $O/plain2_$R.log 2>&1 && \
+  ncu --set full --clock-control none --import-source on -k regex:"mttkrp_fast|nnls_kernel|reduce_partials" -s 8 -c 4 \
+      -f -o $O/prof_$R $CMD > $O/ncu_full_$R.log 2>&1
+echo "full capture rc=$?"
