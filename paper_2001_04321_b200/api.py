@@ -88,6 +88,12 @@ def nnls_solver_from_name(name: str) -> NnlsSolver:
     return table[name]
 
 
+# NTF_RUN_* performance options of AoConfig.flags (include/ntf_b200.h)
+RUN_DIMTREE = 1   # dimension-tree MTTKRP reuse: 2 tensor passes per outer iteration
+RUN_NO_GRAPH = 2  # enqueue every iteration directly (no CUDA graph)
+RUN_GENERIC = 4   # generic MTTKRP kernel only (diagnostics)
+
+
 @dataclasses.dataclass
 class InnerStop:
     """include/ntf/nnls.hpp:20-23."""

@@ -174,13 +174,23 @@ void run_driver(int algo, ntf_ctx* ctx, const ntf_tensor* t, const double* init,
   }
   check_run_inputs(t, init, rank, *cfg);
   const auto shape = int_shape(t);
+  // NTF_TIMING=1: host-side phase times of the driver on stderr (diagnostics)
+  static const bool timing = std::getenv("NTF_TIMING") != nullptr;
+  const auto now = [] { return std::chrono::steady_clock::now(); };
+  const auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+  const auto t0 = now();
   Session s(ctx, t, algo, init, rank, *cfg, params);
+  const auto t1 = now();
   const long long len = model_len(t, rank);
   const bool per_iteration = observer != nullptr || cfg->record_factor_error || cfg->max_time_s > 0.0;
   std::vector<double> e_values;
   if (!per_iteration) {
     s.step(cfg->max_outer_iters);
+    const auto t2 = now();
     s.sync();
+    if (timing)
+      fprintf(stderr, "[ntf timing] session %.2f ms, enqueue %.2f ms, device wait %.2f ms\n", ms(t0, t1), ms(t1, t2),
+              ms(t2, now()));
   } else {
     std::vector<double> acc(static_cast<size_t>(len));
     std::vector<ntf_trace_record> last(1);
@@ -316,6 +326,7 @@ int ntf_ctx_create(int device, ntf_ctx** out) {
     try {
       c->device = device;
       NTF_CUDA(cudaSetDevice(device));
+      retain_pool_memory(device);
       NTF_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
       c->sms = device_sm_count();
       c->scratch = DevBuf(4096 * sizeof(double));
@@ -422,7 +433,10 @@ int ntf_tensor_norm_sq(const ntf_tensor* t, double* out) {
 }
 
 int ntf_tensor_destroy(ntf_tensor* t) {
-  return guarded([&] { delete t; });
+  return guarded([&] {
+    if (t && t->ctx) NTF_CUDA(cudaStreamSynchronize(t->ctx->stream));  // no work may still read it
+    delete t;
+  });
 }
 
 int ntf_mttkrp(ntf_ctx* ctx, const ntf_tensor* t, const double* factors, int rank, int mode, double* out) {

@@ -70,65 +70,72 @@ bool choose(const ModeView& v, int dtype, int sms, Choice* out) {
   if (const char* e = std::getenv("NTF_FAST_NP")) NP = std::max(1, std::atoi(e));  // tuning override
   const int cons_cap = std::min(kMaxMW, warp_cap - NP);
   if (cons_cap < 1) return false;
-  int MW, n_mtiles;
+  int MW0, n_mtiles0;
   if (mw_total <= cons_cap) {
-    MW = int(mw_total);
-    n_mtiles = 1;
+    MW0 = int(mw_total);
+    n_mtiles0 = 1;
   } else {
-    MW = std::min(cons_cap, 8);
-    n_mtiles = int((v.I + (long long)MW * RW - 1) / ((long long)MW * RW));
+    MW0 = std::min(cons_cap, 8);
+    n_mtiles0 = int((v.I + (long long)MW0 * RW - 1) / ((long long)MW0 * RW));
   }
-  // at least four consumer warps (one per SM sub-partition): split k
-  int KW = std::max(1, std::min(8, (4 + MW - 1) / MW));
-  if (const char* e = std::getenv("NTF_FAST_KW")) KW = std::max(1, std::min(8, std::atoi(e)));
-  while (MW * KW > cons_cap && KW > 1) --KW;
-  const int m_cta = MW * RW;
-  fast::Params& p = out->p;
-  p = fast::Params{};
-  p.v = v;
-  p.MW = MW;
-  p.KW = KW;
-  p.NP = NP;
-  p.m_cta = m_cta;
-  p.n_mbox = (m_cta + 255) / 256;
-  p.m_box = m_cta / p.n_mbox;
-  if (p.m_box * p.n_mbox != m_cta || p.m_box % 8) return false;
-  const int vec = int(16 / es);
-  const int bp = (cfg.B + vec - 1) / vec * vec;
-  p.wld = cfg.G * bp;
-  if (layout == fast::kRow) {
-    p.kbox = int(128 / es);
-    p.nbox_r = (v.R + p.kbox - 1) / p.kbox;
-    p.units = v.L * p.nbox_r;
-    p.t_stage_bytes = unsigned(m_cta * 128);
-  } else {
-    p.kbox = int(128 / es);  // 16 doubles / 32 floats of l per unit
-    p.nbox_r = 0;
-    p.units = (v.L + p.kbox - 1) / p.kbox;
-    p.t_stage_bytes = unsigned(size_t(m_cta) * p.kbox * es);
+  // Tall views (the dimension tree's T x_N A_N has I = prod_{n<N-1} I_n rows)
+  // need smaller m-tiles for a pipeline of >= 2 NP stages: fewer m-warps.
+  for (int MW = MW0; MW >= 1; --MW) {
+    const int n_mtiles = MW == MW0 ? n_mtiles0 : int((v.I + (long long)MW * RW - 1) / ((long long)MW * RW));
+    // at least four consumer warps (one per SM sub-partition): split k
+    int KW = std::max(1, std::min(8, (4 + MW - 1) / MW));
+    if (const char* e = std::getenv("NTF_FAST_KW")) KW = std::max(1, std::min(8, std::atoi(e)));
+    while (MW * KW > cons_cap && KW > 1) --KW;
+    const int m_cta = MW * RW;
+    fast::Params& p = out->p;
+    p = fast::Params{};
+    p.v = v;
+    p.MW = MW;
+    p.KW = KW;
+    p.NP = NP;
+    p.m_cta = m_cta;
+    p.n_mbox = (m_cta + 255) / 256;
+    p.m_box = m_cta / p.n_mbox;
+    if (p.m_box * p.n_mbox != m_cta || p.m_box % 8) continue;
+    const int vec = int(16 / es);
+    const int bp = (cfg.B + vec - 1) / vec * vec;
+    p.wld = cfg.G * bp;
+    if (layout == fast::kRow) {
+      p.kbox = int(128 / es);
+      p.nbox_r = (v.R + p.kbox - 1) / p.kbox;
+      p.units = v.L * p.nbox_r;
+      p.t_stage_bytes = unsigned(m_cta * 128);
+    } else {
+      p.kbox = int(128 / es);  // 16 doubles / 32 floats of l per unit
+      p.nbox_r = 0;
+      p.units = (v.L + p.kbox - 1) / p.kbox;
+      p.t_stage_bytes = unsigned(size_t(m_cta) * p.kbox * es);
+    }
+    p.tx_bytes = p.t_stage_bytes;
+    p.w_stage_bytes = unsigned((size_t(p.kbox) * p.wld * es + 127) / 128 * 128);
+    // KB rows of the last varying mode, 2 x kMaxBase base rows, 2 info ints
+    p.aq_stage_bytes =
+        unsigned(((size_t(p.kbox) + 2 * fast::kMaxBase) * v.rank * es + 2 * sizeof(int) + 127) / 128 * 128);
+    const size_t per_stage = size_t(p.t_stage_bytes) + p.w_stage_bytes + p.aq_stage_bytes;
+    p.stages = int(std::min<size_t>(8, kSmemBudget / per_stage));
+    if (const char* e = std::getenv("NTF_FAST_STAGES"))  // tuning override
+      p.stages = std::min(p.stages, std::max(2, std::atoi(e)));
+    // Producer warp w owns stages s == w (mod NP) and visits them in
+    // consecutive rounds, so its parity waits never run more than one phase
+    // ahead of an mbarrier; that needs NP | stages.
+    p.stages -= p.stages % p.NP;
+    if (p.stages < 2 * p.NP) continue;  // each producer looks at least one unit ahead
+    // the k-split fold reuses the T stages as scratch
+    if (size_t(m_cta) * cfg.G * cfg.B * es > size_t(p.stages) * p.t_stage_bytes) continue;
+    p.ctas_per_mtile = int(std::max<long long>(1, std::min<long long>(p.units, std::max(1, sms / n_mtiles))));
+    out->grid = n_mtiles * p.ctas_per_mtile;
+    out->threads = 32 * (p.NP + MW * KW);
+    out->smem = size_t(p.stages) * per_stage + 3 * size_t(p.stages) * sizeof(uint64_t);
+    out->cfg = cfg;
+    out->layout = layout;
+    return true;
   }
-  p.tx_bytes = p.t_stage_bytes;
-  p.w_stage_bytes = unsigned((size_t(p.kbox) * p.wld * es + 127) / 128 * 128);
-  // KB rows of the last varying mode, 2 x kMaxBase base rows, 2 info ints
-  p.aq_stage_bytes = unsigned(((size_t(p.kbox) + 2 * fast::kMaxBase) * v.rank * es + 2 * sizeof(int) + 127) / 128 * 128);
-  const size_t per_stage = size_t(p.t_stage_bytes) + p.w_stage_bytes + p.aq_stage_bytes;
-  p.stages = int(std::min<size_t>(8, kSmemBudget / per_stage));
-  if (const char* e = std::getenv("NTF_FAST_STAGES"))  // tuning override
-    p.stages = std::min(p.stages, std::max(2, std::atoi(e)));
-  // Producer warp w owns stages s == w (mod NP) and visits them in
-  // consecutive rounds, so its parity waits never run more than one phase
-  // ahead of an mbarrier; that needs NP | stages.
-  p.stages -= p.stages % p.NP;
-  if (p.stages < 2 * p.NP) return false;  // each producer looks at least one unit ahead
-  // the k-split fold reuses the T stages as scratch
-  if (size_t(m_cta) * cfg.G * cfg.B * es > size_t(p.stages) * p.t_stage_bytes) return false;
-  p.ctas_per_mtile = int(std::max<long long>(1, std::min<long long>(p.units, std::max(1, sms / n_mtiles))));
-  out->cfg = cfg;
-  out->layout = layout;
-  out->grid = n_mtiles * p.ctas_per_mtile;
-  out->threads = 32 * (p.NP + MW * KW);
-  out->smem = size_t(p.stages) * per_stage + 3 * size_t(p.stages) * sizeof(uint64_t);
-  return true;
+  return false;
 }
 
 void make_map(const void* t, int dtype, const ModeView& v, const Choice& ch, CUtensorMap* map) {
@@ -173,7 +180,11 @@ bool fast_mttkrp_supported(const ModeView& v, int dtype) {
   return choose(v, dtype, device_sm_count(), &ch);
 }
 
-int fast_mttkrp_kernels(const ModeView&, int) { return 2; }
+int fast_mttkrp_kernels(const ModeView& v, int dtype) {
+  Choice ch;
+  if (!choose(v, dtype, device_sm_count(), &ch)) return 2;
+  return ch.p.ctas_per_mtile == 1 ? 1 : 2;
+}
 
 size_t fast_mttkrp_partial_len(const ModeView& v, int dtype, int sms) {
   Choice ch;
@@ -206,6 +217,7 @@ UnitModes unit_modes(const ModeView& v, int layout) {
 void fill_params_modes(const ModeView& v, int layout, fast::Params& p) {
   const UnitModes m = unit_modes(v, layout);
   p.qL = m.qL;
+  if (v.last_factor >= 0 && m.qL == v.order - 1) p.qL = v.last_factor;  // dimension-tree view
   p.nb = m.nb;
   for (int t = 0; t < fast::kMaxBase; ++t) p.bq[t] = m.bq[t];
   p.rowL_wrap = m.qL == 0 ? int(v.row0) : 0;
@@ -276,7 +288,9 @@ void fast_mttkrp(const void* t, int dtype, const ModeView& v, const DevFactors* 
   CUtensorMap map;
   make_map(t, dtype, v, ch, &map);
   ch.p.F = dF;
-  ch.p.partial = partial;
+  // one CTA per m-tile: the kernel writes the result rows directly
+  const bool direct = ch.p.ctas_per_mtile == 1;
+  ch.p.partial = direct ? out : partial;
   ch.p.utab = unit_table;
   fill_params_modes(v, ch.layout, ch.p);
   // diagnostics: NTF_FAST_PROF=1 prints per-CTA-averaged pipeline wait cycles
@@ -302,7 +316,7 @@ void fast_mttkrp(const void* t, int dtype, const ModeView& v, const DevFactors* 
             "consumer %.0f cyc (data wait %.0f) | %.0f cyc/unit\n",
             v.mode, a[5], a[0], a[1], a[2], a[3], a[4], a[5] > 0 ? a[3] / a[5] : 0.0);
   }
-  launch_reduce_partials(partial, ch.p.ctas_per_mtile, v.I * v.rank, out, s);
+  if (!direct) launch_reduce_partials(partial, ch.p.ctas_per_mtile, v.I * v.rank, out, s);
 }
 
 std::string fast_mttkrp_describe(const ModeView& v, int dtype, int sms) {

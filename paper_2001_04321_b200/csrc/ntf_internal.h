@@ -79,7 +79,21 @@ struct ModeView {
   int dims[kMaxOrder];
   long long L, I, R;
   long long row0;
+  int last_factor = -1;  // factor index of the view's last mode when it is not that mode (dimension tree)
 };
+
+// Dimension tree: Y = T x_{N-1} A_{N-1} (modes 0..N-2 of T, r trailing)
+// viewed around block `mode` as (L, I, R, r); see kernels_tree.cu.
+struct TreeView {
+  int order, mode, rank;  // order = N - 1
+  int dims[kMaxOrder];
+  long long L, I, R;
+  long long row0;
+};
+int tree_chunks(const TreeView& v, int sms);
+// out (I x r) = block `mode`'s MTTKRP from Y; partial holds chunks * I * r doubles.
+void launch_tree_mttkrp(const double* Y, const TreeView& v, const DevFactors* dF, double* partial, int chunks,
+                        double* out, cudaStream_t s);
 
 // ---- kernel launchers (CUDA translation units) ------------------------------
 struct MttkrpPlan;

@@ -1,3 +1,6 @@
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 // Host runtime: device buffers, NCCL plumbing, the MTTKRP engine and the
 // GPU-resident HER / AO sessions.
 #include "runtime.h"
@@ -14,15 +17,24 @@
 namespace ntfb {
 
 // ---- DevBuf ------------------------------------------------------------------
+// Device buffers come from the device's stream-ordered memory pool, which
+// the context configures to keep freed memory (release threshold = max):
+// a run's workspaces and a re-uploaded tensor are then served without the
+// driver unmapping and remapping hundreds of MB (cudaFree of a 216 MB
+// tensor measured 1-800 ms on the B200 boxes). Owners synchronise the
+// streams that used a buffer before it is destroyed.
 DevBuf::DevBuf(size_t n) : bytes(n) {
-  if (n) NTF_CUDA(cudaMalloc(&p, n));
+  if (n) {
+    NTF_CUDA(cudaMallocAsync(&p, n, cudaStreamLegacy));
+    NTF_CUDA(cudaStreamSynchronize(cudaStreamLegacy));  // usable from any stream
+  }
 }
 DevBuf::~DevBuf() {
-  if (p) cudaFree(p);
+  if (p) cudaFreeAsync(p, cudaStreamLegacy);
 }
 DevBuf& DevBuf::operator=(DevBuf&& o) noexcept {
   if (this != &o) {
-    if (p) cudaFree(p);
+    if (p) cudaFreeAsync(p, cudaStreamLegacy);
     p = o.p;
     bytes = o.bytes;
     o.p = nullptr;
@@ -50,6 +62,13 @@ void Comm::allgather(double* buf, size_t n_per_rank, cudaStream_t s) const {
 
 Comm::~Comm() {
   if (nccl) ncclCommDestroy(static_cast<ncclComm_t>(nccl));
+}
+
+void retain_pool_memory(int device) {
+  cudaMemPool_t pool;
+  NTF_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+  uint64_t keep = ~0ull;
+  NTF_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
 }
 
 void slab_range(long long dim0, int rank, int world, long long* begin, long long* end) {
@@ -90,6 +109,35 @@ MttkrpEngine::MttkrpEngine(const ntf_ctx* ctx, const ntf_tensor* t, int rank, un
     need = std::max(need, size_t(segs) * size_t(v.I) * rank);
     need = std::max(need, fast_mttkrp_partial_len(v, t->dtype, ctx->sms));
   }
+  if ((flags & NTF_RUN_DIMTREE) && !(flags & NTF_RUN_GENERIC) && t->order >= 3 &&
+      view(t->order - 1).L < (1LL << 31)) {
+    ModeView tv{};
+    tv.order = 2;
+    tv.mode = 0;
+    tv.rank = rank;
+    const ModeView vlast = view(t->order - 1);
+    tv.dims[0] = int(vlast.L);  // rows of the output
+    tv.dims[1] = vlast.dims[t->order - 1];
+    tv.L = 1;
+    tv.I = vlast.L;
+    tv.R = vlast.I;
+    tv.row0 = 0;
+    tv.last_factor = t->order - 1;
+    const std::vector<int> tab = fast_mttkrp_unit_table(tv, t->dtype, ctx->sms);
+    if (!tab.empty()) {
+      tree_ = true;
+      ttm_view_ = tv;
+      ttm_tab_ = DevBuf(tab.size() * sizeof(int));
+      NTF_CUDA(cudaMemcpy(ttm_tab_.p, tab.data(), tab.size() * sizeof(int), cudaMemcpyHostToDevice));
+      ybuf_ = DevBuf(size_t(tv.I) * rank * sizeof(double));
+      need = std::max(need, fast_mttkrp_partial_len(tv, t->dtype, ctx->sms));
+      for (int m = 0; m + 1 < t->order; ++m) {
+        const TreeView yv = tree_view(m);
+        tree_chunks_[m] = tree_chunks(yv, ctx->sms);
+        need = std::max(need, size_t(tree_chunks_[m]) * size_t(yv.I) * rank);
+      }
+    }
+  }
   partial_ = DevBuf(need * sizeof(double));
   if (!(flags & NTF_RUN_GENERIC))
     for (int m = 0; m < t->order; ++m) {
@@ -114,13 +162,34 @@ MttkrpEngine::MttkrpEngine(const ntf_ctx* ctx, const ntf_tensor* t, int rank, un
   }
 }
 
+TreeView MttkrpEngine::tree_view(int mode) const {
+  const ModeView v = view(mode);
+  TreeView y{};
+  y.order = t_->order - 1;
+  y.mode = mode;
+  y.rank = rank_;
+  for (int j = 0; j < y.order; ++j) y.dims[j] = v.dims[j];
+  y.L = 1;
+  y.R = 1;
+  for (int j = 0; j < mode; ++j) y.L *= y.dims[j];
+  y.I = y.dims[mode];
+  for (int j = mode + 1; j < y.order; ++j) y.R *= y.dims[j];
+  y.row0 = t_->row0;
+  return y;
+}
+
 std::string MttkrpEngine::describe(int mode) const {
+  if (tree_ && mode + 1 < t_->order)
+    return std::string("tree chunks=") + std::to_string(tree_chunks_[mode]) +
+           (mode == 0 ? " after TTM " + fast_mttkrp_describe(ttm_view_, t_->dtype, ctx_->sms) : std::string());
   const ModeView v = view(mode);
   if (!(flags_ & NTF_RUN_GENERIC) && fast_mttkrp_supported(v, t_->dtype)) return fast_mttkrp_describe(v, t_->dtype, ctx_->sms);
   return "generic segs=" + std::to_string(segs_[mode]);
 }
 
 int MttkrpEngine::kernels_per_call(int mode) const {
+  if (tree_ && mode + 1 < t_->order)
+    return 2 + (mode == 0 ? fast_mttkrp_kernels(ttm_view_, t_->dtype) : 0);
   const ModeView v = view(mode);
   if (!(flags_ & NTF_RUN_GENERIC) && fast_mttkrp_supported(v, t_->dtype)) return fast_mttkrp_kernels(v, t_->dtype);
   return 2;
@@ -133,7 +202,14 @@ void MttkrpEngine::run(int mode, const DevFactors* dF, double* out, cudaStream_t
   const bool gather = comm.world > 1 && mode == 0;
   double* dst = gather ? gather_.as<double>() + size_t(comm.rank) * maxrows_ * rank_ : out;
   if (ev0) NTF_CUDA(cudaEventRecord(ev0, s));
-  if (unit_tab_[mode].p) {  // a fast plan exists (tables are built only then)
+  if (tree_ && mode + 1 < t_->order) {
+    // block 0 opens the outer iteration: Y with this iteration's A_{N-1}
+    if (mode == 0)
+      fast_mttkrp(t_->data.p, t_->dtype, ttm_view_, dF, ttm_tab_.as<int>(), partial_.as<double>(), ybuf_.as<double>(),
+                  ctx_->sms, s);
+    launch_tree_mttkrp(ybuf_.as<double>(), tree_view(mode), dF, partial_.as<double>(), tree_chunks_[mode], dst, s);
+    if (ev1) NTF_CUDA(cudaEventRecord(ev1, s));
+  } else if (unit_tab_[mode].p) {  // a fast plan exists (tables are built only then)
     fast_mttkrp(t_->data.p, t_->dtype, v, dF, unit_tab_[mode].as<int>(), partial_.as<double>(), dst, ctx_->sms, s);
     if (ev1) NTF_CUDA(cudaEventRecord(ev1, s));
   } else {
@@ -159,13 +235,18 @@ constexpr int kNnlsScratch = 3072 + 64 * kMaxRank * kMaxRank;
 Session::Session(ntf_ctx* ctx, const ntf_tensor* t, int algo, const double* init, int rank,
                  const ntf_ao_config& cfg, const ntf_her_params* params)
     : ctx_(ctx), t_(t), algo_(algo), rank_(rank), order_(t->order), cfg_(cfg) {
+  static const bool timing = std::getenv("NTF_TIMING") != nullptr;
+  const auto now = [] { return std::chrono::steady_clock::now(); };
+  const auto t0 = now();
   NTF_CUDA(cudaSetDevice(ctx->device));
   NTF_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
   for (int i = 0; i < order_; ++i) {
     rows_[i] = int(t->shape[i]);
     total_factor_len_ += (long long)rows_[i] * rank;
   }
+  const auto t1 = now();
   eng_ = std::make_unique<MttkrpEngine>(ctx, t, rank, cfg.flags);
+  const auto t2 = now();
 
   fac_ = DevBuf(size_t(2 * total_factor_len_) * sizeof(double));
   if (t->dtype == NTF_DTYPE_F32) fac32_ = DevBuf(size_t(2 * total_factor_len_) * sizeof(float));
@@ -225,15 +306,18 @@ Session::Session(ntf_ctx* ctx, const ntf_tensor* t, int algo, const double* init
                    stream_);
   NTF_CUDA(cudaMemcpyAsync(&dst->f_prev, &dst->f0, sizeof(double), cudaMemcpyDeviceToDevice, stream_));
   launch_stamp_start(dst, stream_);
-  NTF_CUDA(cudaHostAlloc(&done_host_, sizeof(int), cudaHostAllocDefault));
   NTF_CUDA(cudaStreamSynchronize(stream_));
+  if (timing) {
+    const auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+    fprintf(stderr, "[ntf timing] session: stream %.2f ms, engine %.2f ms, buffers+init+f0 %.2f ms\n",
+            ms(t0, t1), ms(t1, t2), ms(t2, now()));
+  }
 }
 
 Session::~Session() {
   if (exec_) cudaGraphExecDestroy(exec_);
   if (graph_) cudaGraphDestroy(graph_);
   for (auto e : ev_) cudaEventDestroy(e);
-  if (done_host_) cudaFreeHost(done_host_);
   if (stream_) {
     cudaStreamSynchronize(stream_);
     cudaStreamDestroy(stream_);
@@ -332,9 +416,9 @@ int Session::iterations() {
 }
 
 bool Session::done() {
-  NTF_CUDA(cudaMemcpyAsync(done_host_, &state_.as<RunState>()->done, sizeof(int), cudaMemcpyDeviceToHost, stream_));
+  NTF_CUDA(cudaMemcpyAsync(&done_host_, &state_.as<RunState>()->done, sizeof(int), cudaMemcpyDeviceToHost, stream_));
   sync();
-  return *done_host_ != 0;
+  return done_host_ != 0;
 }
 
 void Session::factors(double* out) {

@@ -48,6 +48,8 @@ struct Comm {
 };
 
 void slab_range(long long dim0, int rank, int world, long long* begin, long long* end);
+// Keep freed DevBuf memory in the device's pool (called by context creation).
+void retain_pool_memory(int device);
 
 // ---- MTTKRP engine -------------------------------------------------------------
 // Owns the split-K partial workspace; produces the FULL I_mode x r FP64
@@ -62,6 +64,9 @@ class MttkrpEngine {
   int kernels_per_call(int mode) const;
   ModeView view(int mode) const;
   std::string describe(int mode) const;
+  // Dimension tree (NTF_RUN_DIMTREE, order >= 3, fast plan for the TTM):
+  // run(0) first forms Y = T x_{N-1} A_{N-1}, and blocks 0..N-2 contract Y.
+  bool tree() const { return tree_; }
 
  private:
   const ntf_ctx* ctx_;
@@ -74,6 +79,11 @@ class MttkrpEngine {
   DevBuf slab_meta_;             // begins/counts (long long) per rank
   DevBuf unit_tab_[kMaxOrder];   // fast-path unit tables (empty: generic kernel)
   long long maxrows_ = 0;
+  bool tree_ = false;
+  ModeView ttm_view_{};          // 2-way view (prod_{n<N-1} I_n) x I_{N-1}
+  DevBuf ttm_tab_, ybuf_;        // its unit table; Y (local rows x r, FP64)
+  int tree_chunks_[kMaxOrder] = {};
+  TreeView tree_view(int mode) const;
 };
 
 // ---- GPU-resident solver session ---------------------------------------------
@@ -117,7 +127,7 @@ class Session {
   double kernel_ms_[kMaxOrder] = {};
   int kernel_n_[kMaxOrder] = {};
   int host_iters_ = 0;  // iterations enqueued
-  int* done_host_ = nullptr;  // pinned mirror
+  int done_host_ = 0;  // host mirror of RunState::done
 };
 
 }  // namespace ntfb

@@ -1,0 +1,60 @@
+"""Dimension-tree MTTKRP reuse (NTF_RUN_DIMTREE).
+
+Blocks 0..N-2 of an outer iteration contract Y = T x_{N-1} A_{N-1} instead of
+the tensor; results differ from the direct MTTKRPs only by summation order,
+so the traces must meet the same parity bars against the oracle
+(parity.compare_traces: f_k within 1e-8 relative + the cancellation floor,
+identical restart decisions), for HER and AO, 3-way and 4-way.
+"""
+import numpy as np
+import pytest
+
+from parity import compare_traces, rel_fro
+
+pytestmark = pytest.mark.gpu
+
+
+def _instance(P, shape, rank, sigma, seed):
+    spec = P.SyntheticSpec(shape=shape, rank=rank, noise_sigma=sigma, seed=seed)
+    t, truth = P.generate(spec)
+    init = P.random_init(shape, rank, P.stream_seed(seed, 1))
+    return t, truth, init
+
+
+CASES = [([50, 50, 50], 10, 0.01, 101), ([40, 36, 32], 8, 0.0, 11), ([20, 18, 16, 16], 6, 0.01, 103),
+         ([64, 40, 48], 20, 0.001, 5), ([24, 20, 18, 16], 16, 0.01, 9)]
+
+
+@pytest.mark.parametrize("shape,rank,sigma,seed", CASES)
+def test_dimtree_her_trace_parity(P, oracle, shape, rank, sigma, seed):
+    t, truth, init = _instance(P, shape, rank, sigma, seed)
+    cfg = P.AoConfig(max_outer_iters=50, flags=P.RUN_DIMTREE)
+    model, trace = P.her_run(t, init, cfg, P.HerParams())
+    fo, f0, recs = oracle.run("her", np.asarray(t), init.factors, max_outer_iters=50)
+    stats = compare_traces(trace, f0, recs, oracle.norm_sq(np.asarray(t)))
+    assert stats["checked"] == 50
+    assert model.is_nonnegative()
+
+
+@pytest.mark.parametrize("shape,rank,sigma,seed", CASES[:3])
+def test_dimtree_ao_trace_parity(P, oracle, shape, rank, sigma, seed):
+    t, truth, init = _instance(P, shape, rank, sigma, seed)
+    cfg = P.AoConfig(max_outer_iters=50, flags=P.RUN_DIMTREE)
+    model, trace = P.ao_run(t, init, cfg)
+    fo, f0, recs = oracle.run("ao", np.asarray(t), init.factors, max_outer_iters=50)
+    compare_traces(trace, f0, recs, oracle.norm_sq(np.asarray(t)), check_restarts=False)
+    for a, b in zip(model, fo):
+        assert rel_fro(a, b) < 1e-6
+
+
+@pytest.mark.parametrize("shape,rank", [([300, 300, 300], 20), ([100, 100, 100, 100], 16)], ids=["C2", "C3"])
+def test_dimtree_matches_direct_at_full_size(P, shape, rank):
+    t, truth, init = _instance(P, shape, rank, 0.01, 102)
+    prov = P.GpuDenseProvider(t)
+    _, direct = P.her_run(prov, init, P.AoConfig(max_outer_iters=8), P.HerParams())
+    _, tree = P.her_run(prov, init, P.AoConfig(max_outer_iters=8, flags=P.RUN_DIMTREE), P.HerParams())
+    assert abs(direct.f0 - tree.f0) <= 1e-14 * abs(direct.f0)
+    for a, b in zip(direct.records, tree.records):
+        assert abs(a.f - b.f) <= 1e-10 * abs(a.f) + 64 * 2.0 ** -52 * prov.norm_sq()
+        assert a.restarted == b.restarted
+    prov.close()

@@ -12,42 +12,14 @@ t, truth = P.generate(spec)
 init = P.random_init([300, 300, 300], 20, P.stream_seed(102, 1))
 ctx = P.Context(0)
 t = np.asarray(t)
-
-
-def run(prov, k, tag):
+flags = int(sys.argv[1]) if len(sys.argv) > 1 else 0
+for rep in range(6):
     a = time.perf_counter()
-    m, tr = P.her_run(prov, init, P.AoConfig(max_outer_iters=k), P.HerParams(), ctx=ctx)
+    prov = P.GpuDenseProvider(t, ctx, full_shape=[300, 300, 300])
     b = time.perf_counter()
-    sw = sum(r.inner_sweeps for r in tr.records)
-    print(f"{tag}: her_run {k} iters {1e3 * (b - a):.1f} ms, sweeps {sw}, final f {tr.records[-1].f:.3e}, "
-          f"trace time {tr.records[-1].time_s * 1e3:.1f} ms", flush=True)
-
-
-prov = P.GpuDenseProvider(t, ctx)
-run(prov, 200, "A1")
-run(prov, 200, "A2")
-run(prov, 200, "A3")
-prov.close()
-prov = P.GpuDenseProvider(t, ctx)
-run(prov, 200, "B1")
-run(prov, 200, "B2")
-
-# the bench's sequence: a Session first, then the C-ABI driver
-prov.close()
-prov = P.GpuDenseProvider(t, ctx, full_shape=[300, 300, 300])
-sess = P.Session(prov, init, P.AoConfig(max_outer_iters=10**6), P.HerParams(), algo="her")
-sess.step(10)
-sess.sync()
-sess.step(200)
-sess.sync()
-sess.set_kernel_timing(True)
-sess.step(200)
-sess.sync()
-sess.set_kernel_timing(False)
-sess.close()
-a = time.perf_counter()
-prov2 = P.GpuDenseProvider(t, ctx, full_shape=[300, 300, 300])
-b = time.perf_counter()
-print(f"C upload {1e3 * (b - a):.1f} ms")
-run(prov2, 200, "C1")
-run(prov2, 200, "C2")
+    m, tr = P.her_run(prov, init, P.AoConfig(max_outer_iters=200, flags=flags), P.HerParams(), ctx=ctx)
+    c = time.perf_counter()
+    prov.close()
+    d = time.perf_counter()
+    print(f"rep {rep}: upload {1e3 * (b - a):.1f} ms, her_run {1e3 * (c - b):.1f} ms (device {tr.records[-1].time_s * 1e3:.1f}),"
+          f" close {1e3 * (d - c):.1f} ms", flush=True)
