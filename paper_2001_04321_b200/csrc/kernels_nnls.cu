@@ -643,10 +643,10 @@ void launch_rp(const NnlsLaunch& a, cudaStream_t s) {
     const char* e = std::getenv("NTF_NNLS_Q");
     return e ? std::atoi(e) : 0;
   }();
-  if constexpr (RP >= 12 && RP <= 32) {
+  // measured (tools/tune.py, r01): one lane per row is as fast or faster up
+  // to r = 16 (the triangle is short); from r = 20 four lanes per row win
+  if constexpr (RP >= 20 && RP <= 32) {
     if (qenv != 1 && launch_q<RP, 4, TPB>(a, s)) return;
-  } else if constexpr (RP == 8) {
-    if (qenv != 1 && launch_q<RP, 2, TPB>(a, s)) return;
   }
   if (!launch_q<RP, 1, TPB>(a, s)) throw Unsupported("factor too tall for the fused NNLS kernel");
 }
