@@ -31,32 +31,45 @@ constexpr int kTreeQB = 8;  // q steps per load batch
 
 __global__ void __launch_bounds__(kTreeThreads) tree_mttkrp_kernel(const double* __restrict__ Y, TreeView v,
                                                                    const DevFactors* __restrict__ F,
-                                                                   double* __restrict__ partial, long long qpc) {
+                                                                   double* __restrict__ partial, int qpc) {
   extern __shared__ double wsh[];  // [qpc][r]
+  __shared__ const double* fac[kMaxOrder];
   const int r = v.rank;
-  const long long Q = v.L * v.R;
-  const long long q0 = (long long)blockIdx.x * qpc;
-  const long long q1 = q0 + qpc < Q ? q0 + qpc : Q;
-  const long long pairs = v.I * r;
-  const long long p0 = (long long)blockIdx.y * kTreeTile;
+  // factor pointers of the current roles: one round trip (sel and both
+  // candidate pointers in flight together), then shared by the CTA
+  if (threadIdx.x < unsigned(v.order)) {
+    const int j = threadIdx.x;
+    const int sel = F->sel[j];
+    const double* x0 = F->x[j][0];
+    const double* x1 = F->x[j][1];
+    fac[j] = sel ? x1 : x0;
+  }
+  __syncthreads();
+  // every index below fits 32 bits (checked by the launcher)
+  const int Q = int(v.L * v.R);
+  const int q0 = int(blockIdx.x) * qpc;
+  const int q1 = q0 + qpc < Q ? q0 + qpc : Q;
+  const int I = int(v.I), R = int(v.R);
+  const int pairs = I * r;
+  const int p0 = int(blockIdx.y) * kTreeTile;
 
   // Khatri-Rao rows of the chunk: rho digits over the blocks after n (last
   // fastest), l digits over the blocks before n (block 0 carries the slab
   // offset on a multi-GPU context).
-  for (long long e = threadIdx.x; e < (q1 - q0) * r; e += blockDim.x) {
-    const long long q = q0 + e / r;
-    const int c = int(e % r);
-    long long l = q / v.R, rho = q % v.R;
+  for (int e = threadIdx.x; e < (q1 - q0) * r; e += blockDim.x) {
+    const int q = q0 + e / r;
+    const int c = e % r;
+    int l = q / R, rho = q - (q / R) * R;
     double w = 1.0;
     for (int j = v.order - 1; j > v.mode; --j) {
-      const long long d = rho % v.dims[j];
+      const int d = rho % v.dims[j];
       rho /= v.dims[j];
-      w *= F->x[j][F->sel[j]][d * r + c];
+      w *= fac[j][(long long)d * r + c];
     }
     for (int j = v.mode - 1; j >= 0; --j) {
-      const long long d = l % v.dims[j];
+      const int d = l % v.dims[j];
       l /= v.dims[j];
-      w *= F->x[j][F->sel[j]][(d + (j == 0 ? v.row0 : 0)) * r + c];
+      w *= fac[j][((long long)d + (j == 0 ? v.row0 : 0)) * r + c];
     }
     wsh[e] = w;
   }
@@ -68,25 +81,29 @@ __global__ void __launch_bounds__(kTreeThreads) tree_mttkrp_kernel(const double*
   bool ok[kTreePPT];
 #pragma unroll
   for (int k = 0; k < kTreePPT; ++k) {
-    const long long p = p0 + threadIdx.x + (long long)k * kTreeThreads;
+    const int p = p0 + int(threadIdx.x) + k * kTreeThreads;
     ok[k] = p < pairs;
-    const long long i = ok[k] ? p / r : 0;
-    col[k] = ok[k] ? int(p % r) : 0;
-    yoff[k] = i * v.R * r + col[k];
+    const int i = ok[k] ? p / r : 0;
+    col[k] = ok[k] ? p - i * r : 0;
+    yoff[k] = (long long)i * R * r + col[k];
     acc[k] = 0.0;
   }
-  const long long istride = v.I * v.R * r;  // one step of l
-  // kTreeQB steps of q per batch: kTreeQB * kTreePPT independent loads in
-  // flight per thread (Y streams from L2 / HBM), then the FMAs in q order
-  long long q = q0;
+  const long long istride = (long long)I * R * r;  // one step of l
+  // (l, rho) of q advance by counting, no division in the loop;
+  // kTreeQB steps per batch keep kTreeQB * kTreePPT loads in flight
+  int l = q0 / R, rho = q0 - (q0 / R) * R;
+  int q = q0;
   for (; q + kTreeQB <= q1; q += kTreeQB) {
     double y[kTreeQB][kTreePPT];
 #pragma unroll
     for (int b = 0; b < kTreeQB; ++b) {
-      const long long qq = q + b, l = qq / v.R, rho = qq - l * v.R;
-      const double* yq = Y + l * istride + rho * r;
+      const double* yq = Y + l * istride + (long long)rho * r;
 #pragma unroll
       for (int k = 0; k < kTreePPT; ++k) y[b][k] = ok[k] ? __ldg(yq + yoff[k]) : 0.0;
+      if (++rho == R) {
+        rho = 0;
+        ++l;
+      }
     }
 #pragma unroll
     for (int b = 0; b < kTreeQB; ++b) {
@@ -95,17 +112,34 @@ __global__ void __launch_bounds__(kTreeThreads) tree_mttkrp_kernel(const double*
       for (int k = 0; k < kTreePPT; ++k) acc[k] = fma(y[b][k], wq[col[k]], acc[k]);
     }
   }
-  for (; q < q1; ++q) {
-    const long long l = q / v.R, rho = q - l * v.R;
-    const double* yq = Y + l * istride + rho * r;
-    const double* wq = wsh + (q - q0) * r;
+  {
+    // tail: up to kTreeQB - 1 steps, loads first
+    double y[kTreeQB][kTreePPT];
+    const int nt = q1 - q;
 #pragma unroll
-    for (int k = 0; k < kTreePPT; ++k)
-      if (ok[k]) acc[k] = fma(__ldg(yq + yoff[k]), wq[col[k]], acc[k]);
+    for (int b = 0; b < kTreeQB; ++b) {
+      if (b < nt) {
+        const double* yq = Y + l * istride + (long long)rho * r;
+#pragma unroll
+        for (int k = 0; k < kTreePPT; ++k) y[b][k] = ok[k] ? __ldg(yq + yoff[k]) : 0.0;
+        if (++rho == R) {
+          rho = 0;
+          ++l;
+        }
+      }
+    }
+#pragma unroll
+    for (int b = 0; b < kTreeQB; ++b) {
+      if (b < nt) {
+        const double* wq = wsh + (q + b - q0) * r;
+#pragma unroll
+        for (int k = 0; k < kTreePPT; ++k) acc[k] = fma(y[b][k], wq[col[k]], acc[k]);
+      }
+    }
   }
 #pragma unroll
   for (int k = 0; k < kTreePPT; ++k) {
-    const long long p = p0 + threadIdx.x + (long long)k * kTreeThreads;
+    const int p = p0 + int(threadIdx.x) + k * kTreeThreads;
     if (ok[k]) partial[(long long)blockIdx.x * pairs + p] = acc[k];
   }
 }
@@ -125,6 +159,7 @@ void launch_tree_mttkrp(const double* Y, const TreeView& v, const DevFactors* dF
                         double* out, cudaStream_t s) {
   const long long pairs = v.I * v.rank;
   const long long Q = v.L * v.R;
+  if (Q >= (1LL << 31) || pairs >= (1LL << 31)) throw Unsupported("dimension tree: view too large for 32-bit indexing");
   const long long qpc = (Q + chunks - 1) / chunks;
   const int nchunk = int((Q + qpc - 1) / qpc);
   const size_t smem = size_t(qpc) * v.rank * sizeof(double);
@@ -132,7 +167,7 @@ void launch_tree_mttkrp(const double* Y, const TreeView& v, const DevFactors* dF
   if (smem > 48 * 1024)
     NTF_CUDA(cudaFuncSetAttribute(tree_mttkrp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   const dim3 grid(unsigned(nchunk), unsigned((pairs + kTreeTile - 1) / kTreeTile));
-  tree_mttkrp_kernel<<<grid, kTreeThreads, smem, s>>>(Y, v, dF, partial, qpc);
+  tree_mttkrp_kernel<<<grid, kTreeThreads, smem, s>>>(Y, v, dF, partial, int(qpc));
   NTF_CUDA(cudaGetLastError());
   launch_reduce_partials(partial, nchunk, pairs, out, s);
 }

@@ -83,7 +83,11 @@ bool choose(const ModeView& v, int dtype, int sms, Choice* out) {
   for (int MW = MW0; MW >= 1; --MW) {
     const int n_mtiles = MW == MW0 ? n_mtiles0 : int((v.I + (long long)MW * RW - 1) / ((long long)MW * RW));
     // at least four consumer warps (one per SM sub-partition): split k
-    int KW = std::max(1, std::min(8, (4 + MW - 1) / MW));
+    static const int cons_target = [] {
+      const char* e = std::getenv("NTF_FAST_CONS");  // tuning override
+      return e ? std::max(1, std::atoi(e)) : 4;
+    }();
+    int KW = std::max(1, std::min(8, (cons_target + MW - 1) / MW));
     if (const char* e = std::getenv("NTF_FAST_KW")) KW = std::max(1, std::min(8, std::atoi(e)));
     while (MW * KW > cons_cap && KW > 1) --KW;
     const int m_cta = MW * RW;
@@ -183,7 +187,7 @@ bool fast_mttkrp_supported(const ModeView& v, int dtype) {
 int fast_mttkrp_kernels(const ModeView& v, int dtype) {
   Choice ch;
   if (!choose(v, dtype, device_sm_count(), &ch)) return 2;
-  return ch.p.ctas_per_mtile == 1 ? 1 : 2;
+  return ch.p.ctas_per_mtile == 1 ? 1 : 2;  // upper bound (2 without an arrival counter)
 }
 
 size_t fast_mttkrp_partial_len(const ModeView& v, int dtype, int sms) {
@@ -281,16 +285,20 @@ std::vector<int> fast_mttkrp_unit_table(const ModeView& v, int dtype, int sms) {
 }
 
 void fast_mttkrp(const void* t, int dtype, const ModeView& v, const DevFactors* dF, const int* unit_table,
-                 double* partial, double* out, int sms, cudaStream_t s) {
+                 double* partial, double* out, int sms, cudaStream_t s, unsigned* counter) {
   Choice ch;
   if (!choose(v, dtype, sms, &ch)) throw Unsupported("no fast MTTKRP plan for this view");
   if (!unit_table) throw LogicError("fast MTTKRP needs its unit table");
   CUtensorMap map;
   make_map(t, dtype, v, ch, &map);
   ch.p.F = dF;
-  // one CTA per m-tile: the kernel writes the result rows directly
+  // one CTA per m-tile: the kernel writes the result rows directly;
+  // otherwise it reduces its split-K slabs itself (grid-wide arrival count)
   const bool direct = ch.p.ctas_per_mtile == 1;
   ch.p.partial = direct ? out : partial;
+  ch.p.out = out;
+  ch.p.counter = nullptr;
+  if (!direct && counter && !std::getenv("NTF_FAST_SEPARATE_REDUCE")) ch.p.counter = counter;
   ch.p.utab = unit_table;
   fill_params_modes(v, ch.layout, ch.p);
   // diagnostics: NTF_FAST_PROF=1 prints per-CTA-averaged pipeline wait cycles
@@ -309,14 +317,26 @@ void fast_mttkrp(const void* t, int dtype, const ModeView& v, const DevFactors* 
     NTF_CUDA(cudaMemcpyAsync(h.data(), prof, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
     NTF_CUDA(cudaStreamSynchronize(s));
     double a[fast::kProfSlots] = {};
-    for (int b = 0; b < ch.grid; ++b)
-      for (int q = 0; q < fast::kProfSlots; ++q) a[q] += double(h[size_t(b) * fast::kProfSlots + q]) / ch.grid;
+    unsigned long long g0 = ~0ull, g1 = 0, gs0 = 0, gs1 = ~0ull;
+    double gspan = 0;
+    for (int b = 0; b < ch.grid; ++b) {
+      for (int q = 0; q < 6; ++q) a[q] += double(h[size_t(b) * fast::kProfSlots + q]) / ch.grid;
+      const unsigned long long st = h[size_t(b) * fast::kProfSlots + 6], en = h[size_t(b) * fast::kProfSlots + 7];
+      g0 = std::min(g0, st);
+      g1 = std::max(g1, en);
+      gs0 = std::max(gs0, st);
+      gs1 = std::min(gs1, en);
+      gspan += double(en - st) / ch.grid;
+    }
+    fprintf(stderr, "[fast-prof mode %d] CTA starts spread %.1f us, ends spread %.1f us, avg CTA span %.1f us, "
+            "first start to last end %.1f us\n", v.mode, (gs0 - g0) * 1e-3, (g1 - gs1) * 1e-3, gspan * 1e-3,
+            (g1 - g0) * 1e-3);
     fprintf(stderr,
             "[fast-prof mode %d] units/CTA %.1f | producer %.0f cyc (stage wait %.0f, copy wait %.0f) | "
             "consumer %.0f cyc (data wait %.0f) | %.0f cyc/unit\n",
             v.mode, a[5], a[0], a[1], a[2], a[3], a[4], a[5] > 0 ? a[3] / a[5] : 0.0);
   }
-  if (!direct) launch_reduce_partials(partial, ch.p.ctas_per_mtile, v.I * v.rank, out, s);
+  if (!direct && !ch.p.counter) launch_reduce_partials(partial, ch.p.ctas_per_mtile, v.I * v.rank, out, s);
 }
 
 std::string fast_mttkrp_describe(const ModeView& v, int dtype, int sms) {

@@ -18,8 +18,9 @@ size_t fast_mttkrp_partial_len(const ModeView& v, int dtype, int sms);
 // Host-built per-unit table of the fast path (see mttkrp_fast_launch.h);
 // empty when the view has no fast plan. Depends only on shape and dtype.
 std::vector<int> fast_mttkrp_unit_table(const ModeView& v, int dtype, int sms);
+// `counter` (zeroed device word owned by the caller, used by one stream at a
+// time) enables the in-kernel split-K reduction; nullptr: separate kernel.
 void fast_mttkrp(const void* t, int dtype, const ModeView& v, const DevFactors* dF, const int* unit_table,
-                 double* partial, double* out,
-                 int sms, cudaStream_t s);
+                 double* partial, double* out, int sms, cudaStream_t s, unsigned* counter = nullptr);
 
 }  // namespace ntfb

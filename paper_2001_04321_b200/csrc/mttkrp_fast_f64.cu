@@ -11,8 +11,18 @@ template <typename T, int G, int B, int A, int LAYOUT>
 void launch_impl(const CUtensorMap& map, const Params& p, int grid, int threads, size_t smem, cudaStream_t s) {
   auto fn = mttkrp_fast_kernel<T, G, B, A, LAYOUT>;
   NTF_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-  fn<<<grid, threads, smem, s>>>(map, p);
-  NTF_CUDA(cudaGetLastError());
+  // cooperative: the in-kernel slab reduction waits for every CTA
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(unsigned(grid));
+  cfg.blockDim = dim3(unsigned(threads));
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = p.counter ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  NTF_CUDA(cudaLaunchKernelEx(&cfg, fn, map, p));
 }
 
 #define NTF_CFG(T, G, B, A) KernelCfg{G, B, A, launch_impl<T, G, B, A, kRow>, launch_impl<T, G, B, A, kCol>}

@@ -140,6 +140,11 @@ __global__ void __launch_bounds__(max_threads(A, B), 1) mttkrp_fast_kernel(const
   // diagnostics only: compiled in with -DNTF_FAST_PROFILE=1
   const bool prof_on = NTF_FAST_PROFILE && p.prof != nullptr;
 
+  if (prof_on && threadIdx.x == 0) {
+    unsigned long long g;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+    p.prof[blockIdx.x * kProfSlots + 6] = g;
+  }
   if (threadIdx.x == 0) {
     for (int s = 0; s < stages; ++s) {
       mbar_init(&full[s], 32);
@@ -414,6 +419,9 @@ __global__ void __launch_bounds__(max_threads(A, B), 1) mttkrp_fast_kernel(const
 
     if (prof_on && cw == 0 && lane == 0) {
       p.prof[blockIdx.x * kProfSlots + 3] = clock64() - ct0;
+      unsigned long long g;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+      p.prof[blockIdx.x * kProfSlots + 7] = g;
       p.prof[blockIdx.x * kProfSlots + 4] = cw_full;
       p.prof[blockIdx.x * kProfSlots + 5] = u1 - u0;
     }
@@ -456,6 +464,47 @@ __global__ void __launch_bounds__(max_threads(A, B), 1) mttkrp_fast_kernel(const
             if (c < r) out[row * r + c] = double(acc[i][b]);
           }
         }
+      }
+    }
+    if (p.counter) {
+      // ---------------------------------------------- slab reduction
+      // arrive once every slab row of this CTA is written; wait for all CTAs
+      __threadfence();
+      asm volatile("bar.sync 1, %0;" ::"r"(n_consumers * 32) : "memory");
+      if (cw == 0 && lane == 0) {
+        // sense-reversing grid barrier: counter[0] arrivals, counter[1]
+        // generation; the last arrival resets the count and bumps the
+        // generation (any grid size per launch)
+        unsigned gen;
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(gen) : "l"(p.counter + 1) : "memory");
+        const unsigned old = atomicAdd(p.counter, 1u);
+        if (old == gridDim.x - 1) {
+          p.counter[0] = 0u;
+          asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p.counter + 1), "r"(gen + 1u) : "memory");
+        } else {
+          unsigned seen;
+          do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(p.counter + 1) : "memory");
+          } while (seen == gen);
+        }
+      }
+      asm volatile("bar.sync 1, %0;" ::"r"(n_consumers * 32) : "memory");
+      const long long n = v.I * r;
+      const long long per = (n + gridDim.x - 1) / gridDim.x;
+      const long long e0 = (long long)blockIdx.x * per;
+      const long long e1 = e0 + per < n ? e0 + per : n;
+      const int nsl = p.ctas_per_mtile;
+      for (long long e = e0 + (long long)cw * 32 + lane; e < e1; e += (long long)n_consumers * 32) {
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+        int q = 0;
+        for (; q + 4 <= nsl; q += 4) {
+          s0 += __ldcg(p.partial + (size_t(q) * n + e));
+          s1 += __ldcg(p.partial + (size_t(q + 1) * n + e));
+          s2 += __ldcg(p.partial + (size_t(q + 2) * n + e));
+          s3 += __ldcg(p.partial + (size_t(q + 3) * n + e));
+        }
+        for (; q < nsl; ++q) s0 += __ldcg(p.partial + (size_t(q) * n + e));
+        p.out[e] = (s0 + s1) + (s2 + s3);
       }
     }
   }

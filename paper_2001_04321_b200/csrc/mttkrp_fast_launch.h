@@ -23,13 +23,19 @@ constexpr int kMaxBase = 2;  // fast path: tensors of order <= 4 (others: generi
 constexpr int kUnitInts = 6 + 2 * kMaxBase;
 // prof slots: [0] producer total, [1] producer waiting for a free stage,
 // [2] producer waiting for its copies, [3] consumer total, [4] consumer
-// waiting for a full stage, [5] units
-constexpr int kProfSlots = 6;
+// waiting for a full stage, [5] units, [6] globaltimer at kernel start,
+// [7] globaltimer at the end of the consumer loop
+constexpr int kProfSlots = 8;
 
 struct Params {
   ModeView v;
   const DevFactors* F;
   double* partial;  // [ctas_per_mtile][I][r]
+  // in-kernel slab reduction (ctas_per_mtile > 1): every CTA is resident
+  // (cooperative launch); after a grid-wide arrival count each CTA sums its
+  // share of the outputs over the slabs in slab order into `out`
+  double* out;
+  unsigned* counter;  // [arrivals, generation] of the grid barrier (zeroed once)
   long long units;  // per m-tile
   long long nbox_r; // ROW: rho boxes per l
   int kbox;         // reduction indices per unit
@@ -53,7 +59,7 @@ struct KernelCfg {
 
 // Thread cap of an instantiation: small accumulator tiles allow 16 warps
 // (<= 128 registers), medium ones 12 warps (<= 168), large 8 (<= 255).
-constexpr int max_threads(int A, int B) { return A * B <= 24 ? 512 : (A * B <= 40 ? 384 : 256); }
+constexpr int max_threads(int A, int B) { return A * B <= 24 ? 512 : (A * B <= 50 ? 384 : 256); }
 
 // Picks the blocking for (dtype, rank, rows); false when no instantiation
 // covers the rank.

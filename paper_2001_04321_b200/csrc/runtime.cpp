@@ -139,6 +139,8 @@ MttkrpEngine::MttkrpEngine(const ntf_ctx* ctx, const ntf_tensor* t, int rank, un
     }
   }
   partial_ = DevBuf(need * sizeof(double));
+  counter_ = DevBuf(2 * sizeof(unsigned));
+  NTF_CUDA(cudaMemset(counter_.p, 0, 2 * sizeof(unsigned)));
   if (!(flags & NTF_RUN_GENERIC))
     for (int m = 0; m < t->order; ++m) {
       const std::vector<int> tab = fast_mttkrp_unit_table(view(m), t->dtype, ctx->sms);
@@ -188,10 +190,14 @@ std::string MttkrpEngine::describe(int mode) const {
 }
 
 int MttkrpEngine::kernels_per_call(int mode) const {
+  // the fast kernel reduces its split-K slabs itself (the engine passes an
+  // arrival counter) unless NTF_FAST_SEPARATE_REDUCE asks for the old kernel
+  const int fast_kernels = std::getenv("NTF_FAST_SEPARATE_REDUCE") ? 2 : 1;
   if (tree_ && mode + 1 < t_->order)
-    return 2 + (mode == 0 ? fast_mttkrp_kernels(ttm_view_, t_->dtype) : 0);
+    return 2 + (mode == 0 ? std::min(fast_kernels, fast_mttkrp_kernels(ttm_view_, t_->dtype)) : 0);
   const ModeView v = view(mode);
-  if (!(flags_ & NTF_RUN_GENERIC) && fast_mttkrp_supported(v, t_->dtype)) return fast_mttkrp_kernels(v, t_->dtype);
+  if (!(flags_ & NTF_RUN_GENERIC) && fast_mttkrp_supported(v, t_->dtype))
+    return std::min(fast_kernels, fast_mttkrp_kernels(v, t_->dtype));
   return 2;
 }
 
@@ -206,11 +212,12 @@ void MttkrpEngine::run(int mode, const DevFactors* dF, double* out, cudaStream_t
     // block 0 opens the outer iteration: Y with this iteration's A_{N-1}
     if (mode == 0)
       fast_mttkrp(t_->data.p, t_->dtype, ttm_view_, dF, ttm_tab_.as<int>(), partial_.as<double>(), ybuf_.as<double>(),
-                  ctx_->sms, s);
+                  ctx_->sms, s, counter_.as<unsigned>());
     launch_tree_mttkrp(ybuf_.as<double>(), tree_view(mode), dF, partial_.as<double>(), tree_chunks_[mode], dst, s);
     if (ev1) NTF_CUDA(cudaEventRecord(ev1, s));
   } else if (unit_tab_[mode].p) {  // a fast plan exists (tables are built only then)
-    fast_mttkrp(t_->data.p, t_->dtype, v, dF, unit_tab_[mode].as<int>(), partial_.as<double>(), dst, ctx_->sms, s);
+    fast_mttkrp(t_->data.p, t_->dtype, v, dF, unit_tab_[mode].as<int>(), partial_.as<double>(), dst, ctx_->sms, s,
+                counter_.as<unsigned>());
     if (ev1) NTF_CUDA(cudaEventRecord(ev1, s));
   } else {
     launch_mttkrp_generic(t_->data.p, t_->dtype, v, dF, partial_.as<double>(), segs_[mode], s);

@@ -82,6 +82,7 @@ class MttkrpEngine {
   bool tree_ = false;
   ModeView ttm_view_{};          // 2-way view (prod_{n<N-1} I_n) x I_{N-1}
   DevBuf ttm_tab_, ybuf_;        // its unit table; Y (local rows x r, FP64)
+  DevBuf counter_;               // arrival counter of the in-kernel split-K reduction
   int tree_chunks_[kMaxOrder] = {};
   TreeView tree_view(int mode) const;
 };
