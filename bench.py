@@ -2,11 +2,14 @@
 """HER-AHALS outer iterations/s on BASELINE config 2 (300^3, r=20, FP64).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                  [--config c2|c3|c4|c1]
+                  [--config c2|c3|c4|c1] [--no-dimtree]
 
-A "step" is one HER-AHALS outer iteration (N MTTKRPs + N fused AHALS /
+A "step" is one HER-AHALS outer iteration (N block MTTKRPs + N fused AHALS /
 extrapolation / Gram updates + the on-device restart decision) over the full
-synthetic instance. ``value`` is device-timed (CUDA events on the session
+synthetic instance. By default the block MTTKRPs use the dimension tree
+(one T x_{N-1} A_{N-1} pass shared by blocks 0..N-2, one full pass for block
+N-1; identical algorithm, summation order only); --no-dimtree runs N full
+passes. ``value`` is device-timed (CUDA events on the session
 stream, tensor resident in HBM; the 216 MB tensor exceeds the 126 MB L2, so no
 flush is needed). ``e2e`` is the same metric through the public C-ABI driver
 ntf_her_run with host buffers: upload of the tensor and init, K iterations,
@@ -219,7 +222,13 @@ def run_ours(args):
     trace = sess.trace()
     n_modes = len(shape)
     per_mode_ms = [kms[i] / max(kcnt[i], 1) for i in range(n_modes)]
-    avg_ms = sum(kms) / max(sum(kcnt), 1)
+    # the roofline kernel is a full MTTKRP pass: every mode without the
+    # dimension tree; with it only block N-1 is one (blocks 0..N-2 contract
+    # Y, block 0 after the T x_{N-1} A_{N-1} pass) -- per_mode_ms shows all
+    if args.dimtree:
+        avg_ms = per_mode_ms[-1]
+    else:
+        avg_ms = sum(kms) / max(sum(kcnt), 1)
     local_shape = list(t_local.shape)
     bytes_per = P.mttkrp_bytes(local_shape, r, itemsize)
     flops_per = P.mttkrp_flops(local_shape, r)
@@ -276,7 +285,8 @@ def run_ours(args):
             "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm_peak, "unit": "GB/s",
                          "frac": achieved_gbs / hbm_peak, "traffic": traffic, "peak_kind": peak_kind,
                          "traffic_source": "profiles/traffic.json (ncu dram__bytes_read+write per launch)",
-                         "kernel": "MTTKRP (main kernel, avg over modes)",
+                         "kernel": ("MTTKRP full pass of block N-1 (dimension tree on)" if args.dimtree
+                                    else "MTTKRP (main kernel, avg over modes)"),
                          "bytes_per_launch": bytes_per, "avg_launch_ms": avg_ms,
                          "per_mode_ms": per_mode_ms,
                          "fma_tflops": flops_per / (avg_ms / 1e3) / 1e12,
@@ -303,7 +313,10 @@ def main():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
-    ap.add_argument("--dimtree", action="store_true")
+    # dimension-tree reuse (NTF_RUN_DIMTREE) is the production path: same
+    # algorithm, 2 full tensor passes per outer iteration instead of N
+    ap.add_argument("--dimtree", dest="dimtree", action="store_true", default=True)
+    ap.add_argument("--no-dimtree", dest="dimtree", action="store_false")
     ap.add_argument("--cpu-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
