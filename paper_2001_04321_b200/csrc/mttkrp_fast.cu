@@ -66,7 +66,11 @@ bool choose(const ModeView& v, int dtype, int sms, Choice* out) {
   const int RW = (32 / cfg.G) * cfg.A;
   const long long mw_total = (v.I + RW - 1) / RW;
   const int warp_cap = fast::max_threads(cfg.A, cfg.B) / 32;
-  int NP = 2;  // producer warps (each forms W for every NP-th unit)
+  // producer warps (each forms W for every NP-th unit): a short m range
+  // (<= 128 rows, e.g. C3) means small units, so W formation and copy
+  // issue, not the FMAs, bound the pipeline (r01: 4 producers 245 us vs
+  // 2 producers 339 us per C3 mode)
+  int NP = RW * mw_total <= 128 ? 4 : 2;
   if (const char* e = std::getenv("NTF_FAST_NP")) NP = std::max(1, std::atoi(e));  // tuning override
   const int cons_cap = std::min(kMaxMW, warp_cap - NP);
   if (cons_cap < 1) return false;
@@ -83,10 +87,8 @@ bool choose(const ModeView& v, int dtype, int sms, Choice* out) {
   for (int MW = MW0; MW >= 1; --MW) {
     const int n_mtiles = MW == MW0 ? n_mtiles0 : int((v.I + (long long)MW * RW - 1) / ((long long)MW * RW));
     // at least four consumer warps (one per SM sub-partition): split k
-    static const int cons_target = [] {
-      const char* e = std::getenv("NTF_FAST_CONS");  // tuning override
-      return e ? std::max(1, std::atoi(e)) : 4;
-    }();
+    const char* ce = std::getenv("NTF_FAST_CONS");  // tuning override
+    const int cons_target = ce ? std::max(1, std::atoi(ce)) : cfg.cons;
     int KW = std::max(1, std::min(8, (cons_target + MW - 1) / MW));
     if (const char* e = std::getenv("NTF_FAST_KW")) KW = std::max(1, std::min(8, std::atoi(e)));
     while (MW * KW > cons_cap && KW > 1) --KW;

@@ -29,8 +29,8 @@ void launch_impl(const CUtensorMap& map, const Params& p, int grid, int threads,
 
 // Blocking per rank. Shared-memory bytes per DFMA are 8 (A + B) / (A B)
 // (T and W values delivered per lane), and the SM moves 128 B/clk against 64
-// DFMA/clk, so the production shapes keep A*B/(A+B) near 5 (C2: 10x10,
-// C3: 7x8) and split k across warps to keep four consumer warps.
+// DFMA/clk, so the shapes keep A*B/(A+B) near 3-5 and split k across warps
+// to keep four (or, with smaller tiles, eight) consumer warps.
 bool lookup_f64(int r, long long rows, KernelCfg* out) {
   if (const char* e = std::getenv("NTF_FAST_ALT")) {  // tuning: alternative blockings
     const int alt = std::atoi(e);
@@ -43,7 +43,12 @@ bool lookup_f64(int r, long long rows, KernelCfg* out) {
   else if (r <= 10) *out = NTF_CFG(double, 2, 5, 4);
   else if (r <= 12) *out = NTF_CFG(double, 2, 6, 6);
   else if (r <= 16) *out = (rows > 64 && rows <= 112) ? NTF_CFG(double, 2, 8, 7) : NTF_CFG(double, 2, 8, 8);
-  else if (r <= 20) *out = NTF_CFG(double, 2, 10, 10);
+  else if (r <= 20) {
+    // measured (r01, C2): 8 consumer warps of 8 x 5 tiles beat 4 of 10 x 10
+    // on every mode, and the COL layout most (80 vs 100 us)
+    *out = NTF_CFG(double, 4, 5, 8);
+    out->cons = 8;
+  }
   else if (r <= 24) *out = NTF_CFG(double, 2, 12, 8);
   else if (r <= 32) *out = NTF_CFG(double, 4, 8, 8);
   else if (r <= 64) *out = NTF_CFG(double, 8, 8, 8);

@@ -55,6 +55,7 @@ using LaunchFn = void (*)(const CUtensorMap& map, const Params& p, int grid, int
 struct KernelCfg {
   int G, B, A;
   LaunchFn row, col;
+  int cons = 4;  // target consumer warps per CTA (8: two per SM sub-partition)
 };
 
 // Thread cap of an instantiation: small accumulator tiles allow 16 warps
