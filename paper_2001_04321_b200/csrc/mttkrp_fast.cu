@@ -65,7 +65,7 @@ bool choose(const ModeView& v, int dtype, int sms, Choice* out) {
   if (!fast::lookup(dtype, v.rank, v.I, &cfg)) return false;
   const int RW = (32 / cfg.G) * cfg.A;
   const long long mw_total = (v.I + RW - 1) / RW;
-  const int warp_cap = fast::max_threads(cfg.A, cfg.B) / 32;
+  const int warp_cap = fast::max_threads_es(cfg.A, cfg.B, int(es)) / 32;
   // producer warps (each forms W for every NP-th unit): a short m range
   // (<= 128 rows, e.g. C3) means small units, so W formation and copy
   // issue, not the FMAs, bound the pipeline (r01: 4 producers 245 us vs

@@ -1,5 +1,7 @@
 // FP32 instantiations of the fast MTTKRP kernel (FFMA on CUDA cores; the
 // per-CTA partials are written in FP64 and reduced in FP64).
+#include <cstdlib>
+
 #include "mttkrp_fast_impl.cuh"
 #include "mttkrp_fast_launch.h"
 
@@ -27,12 +29,18 @@ void launch_impl32(const CUtensorMap& map, const Params& p, int grid, int thread
 #define NTF_CFG32(G, B, A) KernelCfg{G, B, A, launch_impl32<float, G, B, A, kRow>, launch_impl32<float, G, B, A, kCol>}
 
 bool lookup_f32(int r, long long, KernelCfg* out) {
+  if (const char* e = std::getenv("NTF_FAST_ALT")) {  // tuning: alternative blockings
+    const int alt = std::atoi(e);
+    if (r > 20 && r <= 32 && alt == 1) return *out = NTF_CFG32(4, 8, 8), true;
+    if (r > 20 && r <= 32 && alt == 2) return *out = NTF_CFG32(2, 16, 8), true;
+    if (r > 20 && r <= 32 && alt == 3) return *out = NTF_CFG32(4, 8, 6), true;
+  }
   if (r <= 4) *out = NTF_CFG32(2, 2, 4);
   else if (r <= 8) *out = NTF_CFG32(2, 4, 4);
   else if (r <= 12) *out = NTF_CFG32(2, 6, 4);
   else if (r <= 16) *out = NTF_CFG32(2, 8, 4);
   else if (r <= 20) *out = NTF_CFG32(4, 5, 4);
-  else if (r <= 32) *out = NTF_CFG32(4, 8, 4);
+  else if (r <= 32) *out = NTF_CFG32(2, 16, 8);  // r01 C4 sweep: best of 4x8x4, 4x8x8, 2x16x8, 4x8x6
   else if (r <= 64) *out = NTF_CFG32(8, 8, 8);
   else return false;
   return true;

@@ -110,7 +110,7 @@ __device__ __forceinline__ const float* factor_ptr<float>(const DevFactors* F, i
 // G column groups of B columns each (padded to BP so 16-byte loads stay
 // aligned); RG = 32/G row groups; A rows per lane.
 template <typename T, int G, int B, int A, int LAYOUT>
-__global__ void __launch_bounds__(max_threads(A, B), 1) mttkrp_fast_kernel(const __grid_constant__ CUtensorMap tmap, Params p) {
+__global__ void __launch_bounds__(max_threads_es(A, B, int(sizeof(T))), 1) mttkrp_fast_kernel(const __grid_constant__ CUtensorMap tmap, Params p) {
   using VT = Vec<T>;
   using V = typename VT::V;
   constexpr int VEC = VT::N;

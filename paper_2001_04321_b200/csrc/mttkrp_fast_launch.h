@@ -61,6 +61,8 @@ struct KernelCfg {
 // Thread cap of an instantiation: small accumulator tiles allow 16 warps
 // (<= 128 registers), medium ones 12 warps (<= 168), large 8 (<= 255).
 constexpr int max_threads(int A, int B) { return A * B <= 24 ? 512 : (A * B <= 50 ? 384 : 256); }
+// FP32 accumulators take one register instead of two.
+constexpr int max_threads_es(int A, int B, int es) { return es == 4 ? max_threads(A, (B + 1) / 2) : max_threads(A, B); }
 
 // Picks the blocking for (dtype, rank, rows); false when no instantiation
 // covers the rank.
