@@ -136,6 +136,15 @@ int ntf_random_init(const int* shape, int order, int rank, uint64_t seed, double
  * the FP64 instance rounded to nearest); truth_out: sum(shape)*rank doubles. */
 int ntf_generate(const int* shape, int order, int rank, double sigma, int ill_conditioned,
                  int collinear, uint64_t seed, int dtype, void* tensor_out, double* truth_out);
+/* generate restricted to the mode-1 slab [slab_begin, slab_end) (the rows a
+ * rank of a sharded context owns, ntf_slab_range): tensor_out receives
+ * (slab_end - slab_begin) * prod(shape[1:]) values, bit-identical to that
+ * slab of ntf_generate's tensor (the noise stream is entered at the slab's
+ * first entry); truth_out is the full truth. No reference counterpart: the
+ * reference generates whole instances (datagen.cpp:48-70). */
+int ntf_generate_slab(const int* shape, int order, int rank, double sigma, int ill_conditioned,
+                      int collinear, uint64_t seed, int dtype, int64_t slab_begin, int64_t slab_end,
+                      void* tensor_out, double* truth_out);
 /* factor_error (src/metrics.cpp:79-111). */
 int ntf_factor_error(const double* est, const double* truth, const int* shape, int order, int rank,
                      double* out);

@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libntf_b200.so")
+# NTF_B200_LIB: a diagnostics build (e.g. -DNTF_NNLS_PROFILE=1) of the same library
+LIB_PATH = os.environ.get("NTF_B200_LIB") or os.path.join(_HERE, "libntf_b200.so")
 
 NTF_OK = 0
 NTF_ERR_INVALID_ARGUMENT = 1
@@ -71,6 +72,8 @@ SIGNATURES = {
     "ntf_random_init": (C.c_int, [iptr, C.c_int, C.c_int, C.c_uint64, dptr]),
     "ntf_generate": (C.c_int, [iptr, C.c_int, C.c_int, C.c_double, C.c_int, C.c_int, C.c_uint64, C.c_int,
                                C.c_void_p, dptr]),
+    "ntf_generate_slab": (C.c_int, [iptr, C.c_int, C.c_int, C.c_double, C.c_int, C.c_int, C.c_uint64, C.c_int,
+                                    C.c_int64, C.c_int64, C.c_void_p, dptr]),
     "ntf_factor_error": (C.c_int, [dptr, dptr, iptr, C.c_int, C.c_int, dptr]),
     "ntf_device_count": (C.c_int, [iptr]),
     "ntf_ctx_create": (C.c_int, [C.c_int, C.POINTER(C.c_void_p)]),

@@ -291,22 +291,34 @@ def random_init(shape, rank, seed) -> KruskalModel:
     return KruskalModel.from_flat(out, shape, rank)
 
 
-def generate(spec: SyntheticSpec, dtype=np.float64):
-    """src/datagen.cpp:48-70 -> (tensor ndarray, truth KruskalModel)."""
+def generate(spec: SyntheticSpec, dtype=np.float64, slab=None):
+    """src/datagen.cpp:48-70 -> (tensor ndarray, truth KruskalModel).
+
+    ``slab=(b, e)`` returns only the mode-1 rows [b, e) of the tensor (the
+    part a rank of a sharded context holds), bit-identical to that slice of
+    the whole instance; the truth is always whole."""
     shape = [int(d) for d in spec.shape]
     if not shape:
         raise InvalidArgument("tensor shape must have order >= 1")
     dtype = np.dtype(dtype)
     code = L.NTF_DTYPE_F32 if dtype == np.float32 else L.NTF_DTYPE_F64
-    n = 1
-    for d in shape:
+    b, e = (0, shape[0]) if slab is None else (int(slab[0]), int(slab[1]))
+    if not 0 <= b <= e <= shape[0]:
+        raise InvalidArgument("slab outside the first mode")
+    n = e - b
+    for d in shape[1:]:
         n *= max(d, 0)
-    t = np.empty(n, dtype=np.float32 if code == L.NTF_DTYPE_F32 else np.float64)
+    t = np.empty(max(n, 0), dtype=np.float32 if code == L.NTF_DTYPE_F32 else np.float64)
     truth = np.empty(max(sum(shape) * max(spec.rank, 0), 1))
-    _check(L.lib().ntf_generate((C.c_int * len(shape))(*shape), len(shape), spec.rank, spec.noise_sigma,
-                                int(spec.ill_conditioned), int(spec.collinear), spec.seed, code,
-                                t.ctypes.data_as(C.c_void_p), _dp(truth)))
-    return t.reshape(shape), KruskalModel.from_flat(truth, shape, spec.rank)
+    sh = (C.c_int * len(shape))(*shape)
+    if slab is None:
+        _check(L.lib().ntf_generate(sh, len(shape), spec.rank, spec.noise_sigma, int(spec.ill_conditioned),
+                                    int(spec.collinear), spec.seed, code, t.ctypes.data_as(C.c_void_p), _dp(truth)))
+    else:
+        _check(L.lib().ntf_generate_slab(sh, len(shape), spec.rank, spec.noise_sigma, int(spec.ill_conditioned),
+                                         int(spec.collinear), spec.seed, code, b, e, t.ctypes.data_as(C.c_void_p),
+                                         _dp(truth)))
+    return t.reshape([e - b] + shape[1:]), KruskalModel.from_flat(truth, shape, spec.rank)
 
 
 def factor_error(est, truth) -> float:

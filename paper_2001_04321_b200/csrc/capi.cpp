@@ -293,6 +293,20 @@ int ntf_generate(const int* shape, int order, int rank, double sigma, int ill_co
   });
 }
 
+int ntf_generate_slab(const int* shape, int order, int rank, double sigma, int ill_conditioned, int collinear,
+                      uint64_t seed, int dtype, int64_t slab_begin, int64_t slab_end, void* tensor_out,
+                      double* truth_out) {
+  return guarded([&] {
+    need(shape, "shape");
+    need(tensor_out, "tensor_out");
+    need(truth_out, "truth_out");
+    if (order < 1 || slab_begin < 0 || slab_end < slab_begin || slab_end > shape[0])
+      throw InvalidArgument("slab outside the first mode");
+    generate(shape, order, rank, sigma, ill_conditioned, collinear, seed, dtype, tensor_out, truth_out,
+             (long long)slab_begin, (long long)slab_end);
+  });
+}
+
 int ntf_factor_error(const double* est, const double* truth, const int* shape, int order, int rank, double* out) {
   return guarded([&] {
     need(est, "est");

@@ -7,10 +7,12 @@
 // flat order from sub-stream N. It is inherently sequential in the noise
 // stream, so it stays on the host; the reconstruction part is parallel.
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstring>
 #include <limits>
 #include <random>
+#include <thread>
 #include <vector>
 
 #include "ntf_internal.h"
@@ -75,7 +77,7 @@ void random_init(const int* shape, int order, int rank, uint64_t seed, double* o
 // config 4): A_i[:,j] = 0.5 s_i + 0.5 U_i[:,j], s_i from sub-stream N+1+i.
 template <typename T>
 static void generate_impl(const std::vector<int>& s, int rank, double sigma, bool ill, bool collinear,
-                          uint64_t seed, T* tensor, double* truth) {
+                          uint64_t seed, T* tensor, double* truth, long long slab_b, long long slab_e) {
   const int n = int(s.size());
   std::vector<const double*> A(static_cast<size_t>(n));
   long long off = 0;
@@ -98,57 +100,99 @@ static void generate_impl(const std::vector<int>& s, int rank, double sigma, boo
     A[size_t(i)] = a;
     off += (long long)rows * rank;
   }
-  // Leading-mode Khatri-Rao rows, product from the last listed factor down
-  // to the first (kernels.cpp:104-109), computed per row on the fly.
-  long long lead = 1;
-  for (int i = 0; i + 1 < n; ++i) lead *= s[size_t(i)];
+  // The tensor entries of the mode-1 slab [slab_b, slab_e): flat range
+  // [f0, f1). Entry e = T_rec[e] (Khatri-Rao row of the leading modes, product
+  // from the last listed factor down to the first, kernels.cpp:104-109, dotted
+  // with A_last's row in ascending p), then max(0, . + sigma N(0,1)) with
+  // the Box-Muller pair drawn from noise draws 2e, 2e+1 of sub-stream N
+  // (exactly two draws per entry, no rejection). The noise stream is serial,
+  // so one producer thread walks it (discard) and snapshots the engine at
+  // every chunk start while OpenMP workers reconstruct and add the noise of
+  // whole chunks from their snapshot: same draws, same arithmetic, any
+  // thread count.
+  long long stride0 = 1;
+  for (int i = 1; i < n; ++i) stride0 *= s[size_t(i)];
   const int last = s[size_t(n - 1)];
-  const double* An = A[size_t(n - 1)];
-  std::mt19937_64 noise(stream_seed(seed, uint64_t(n)));
-  const long long chunk = 4096;
-  std::vector<double> buf;
-  for (long long r0 = 0; r0 < lead; r0 += chunk) {
-    const long long r1 = std::min(lead, r0 + chunk);
-    buf.assign(size_t((r1 - r0) * last), 0.0);
-#pragma omp parallel for schedule(static)
-    for (long long row = r0; row < r1; ++row) {
-      double kr[kMaxRank * 4];
-      std::vector<double> krv;
-      double* w = kr;
-      if (rank > kMaxRank * 4) {
-        krv.resize(size_t(rank));
-        w = krv.data();
+  const long long f0 = slab_b * stride0, f1 = slab_e * stride0;
+  const long long count = f1 - f0;
+  if (count <= 0) return;
+  // A_last transposed (p-major): the chunk loop runs over columns innermost,
+  // which keeps each entry's ascending-p sum while vectorising across entries
+  std::vector<double> AnT(size_t(rank) * size_t(last));
+  for (int col = 0; col < last; ++col)
+    for (int p = 0; p < rank; ++p) AnT[size_t(p) * last + col] = A[size_t(n - 1)][(long long)col * rank + p];
+  const long long chunk = 1LL << 20;
+  const long long nchunks = (count + chunk - 1) / chunk;
+  const bool noisy = sigma > 0.0;
+  std::vector<std::mt19937_64> snaps;
+  std::atomic<long long> ready{0};
+  std::thread producer;
+  if (noisy) {
+    snaps.resize(size_t(nchunks));
+    producer = std::thread([&] {
+      std::mt19937_64 g(stream_seed(seed, uint64_t(n)));
+      g.discard(2ull * uint64_t(f0));
+      for (long long c = 0; c < nchunks; ++c) {
+        snaps[size_t(c)] = g;
+        ready.store(c + 1, std::memory_order_release);
+        if (c + 1 < nchunks) g.discard(2ull * uint64_t(chunk));
       }
-      for (int p = 0; p < rank; ++p) w[p] = 1.0;
-      long long rest = row;
-      for (int l = n - 2; l >= 0; --l) {
-        const long long j = rest % s[size_t(l)];
-        rest /= s[size_t(l)];
-        for (int p = 0; p < rank; ++p) w[p] *= A[size_t(l)][j * rank + p];
+    });
+  }
+#pragma omp parallel
+  {
+    std::vector<double> buf(static_cast<size_t>(chunk)), w(static_cast<size_t>(rank));
+#pragma omp for schedule(dynamic, 1)
+    for (long long c = 0; c < nchunks; ++c) {
+      const long long a = f0 + c * chunk, z = std::min(f1, a + chunk);
+      for (long long e = a; e < z;) {
+        const long long row = e / last;  // leading-mode row
+        const int c0 = int(e - row * last);
+        const int c1 = int(std::min<long long>(last, c0 + (z - e)));
+        for (int p = 0; p < rank; ++p) w[size_t(p)] = 1.0;
+        long long rest = row;
+        for (int l = n - 2; l >= 0; --l) {
+          const long long j = rest % s[size_t(l)];
+          rest /= s[size_t(l)];
+          for (int p = 0; p < rank; ++p) w[size_t(p)] *= A[size_t(l)][j * rank + p];
+        }
+        double* out = buf.data() + (e - a) - c0;
+        for (int col = c0; col < c1; ++col) out[col] = 0.0;
+        for (int p = 0; p < rank; ++p) {
+          const double wp = w[size_t(p)];
+          const double* an = AnT.data() + size_t(p) * last;
+          for (int col = c0; col < c1; ++col) out[col] += wp * an[col];
+        }
+        e += c1 - c0;
       }
-      for (int col = 0; col < last; ++col) {
-        double v = 0.0;
-        for (int p = 0; p < rank; ++p) v += w[p] * An[(long long)col * rank + p];
-        buf[size_t((row - r0) * last + col)] = v;
+      T* dst = tensor + (a - f0);
+      if (noisy) {
+        while (ready.load(std::memory_order_acquire) <= c) std::this_thread::yield();
+        std::mt19937_64 g = snaps[size_t(c)];
+        for (long long e = 0; e < z - a; ++e) dst[e] = T(std::max(0.0, buf[size_t(e)] + sigma * gauss_draw(g)));
+      } else {
+        for (long long e = 0; e < z - a; ++e) dst[e] = T(buf[size_t(e)]);
       }
-    }
-    for (long long e = 0; e < (r1 - r0) * last; ++e) {
-      double v = buf[size_t(e)];
-      if (sigma > 0.0) v = std::max(0.0, v + sigma * gauss_draw(noise));
-      tensor[r0 * last + e] = T(v);
     }
   }
+  if (producer.joinable()) producer.join();
 }
 
 void generate(const int* shape, int order, int rank, double sigma, int ill, int collinear, uint64_t seed,
-              int dtype, void* tensor, double* truth) {
+              int dtype, void* tensor, double* truth, long long slab_b, long long slab_e) {
   const auto s = check_shape(shape, order, rank);
   if (sigma < 0.0) throw InvalidArgument("noise level must be >= 0");
   if (ill && rank < 2) throw InvalidArgument("ill-conditioned instances need rank >= 2");
+  if (slab_b < 0 && slab_e < 0) {
+    slab_b = 0;
+    slab_e = s[0];
+  }
+  if (slab_b < 0 || slab_e < slab_b || slab_e > s[0]) throw InvalidArgument("slab outside the first mode");
   if (dtype == NTF_DTYPE_F32)
-    generate_impl(s, rank, sigma, ill != 0, collinear != 0, seed, static_cast<float*>(tensor), truth);
+    generate_impl(s, rank, sigma, ill != 0, collinear != 0, seed, static_cast<float*>(tensor), truth, slab_b, slab_e);
   else if (dtype == NTF_DTYPE_F64)
-    generate_impl(s, rank, sigma, ill != 0, collinear != 0, seed, static_cast<double*>(tensor), truth);
+    generate_impl(s, rank, sigma, ill != 0, collinear != 0, seed, static_cast<double*>(tensor), truth, slab_b,
+                  slab_e);
   else
     throw InvalidArgument("unknown dtype");
 }

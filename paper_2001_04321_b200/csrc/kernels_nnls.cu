@@ -651,6 +651,675 @@ void launch_rp(const NnlsLaunch& a, cudaStream_t s) {
   if (!launch_q<RP, 1, TPB>(a, s)) throw Unsupported("factor too tall for the fused NNLS kernel");
 }
 
+
+// ===========================================================================
+// Stream AHALS (r <= 32): the column updates of all sweeps form one stream
+// t = s * RP + j. Every evaluation of column j pushes the new W[j] into the
+// pending sums of all other columns, so the "triangle" of a Gauss-Seidel
+// pass (the sum over W_old[l > j]) is never formed at the pass start:
+//
+//   P_q  = C_q / G_qq - sum_{l != q} (G_lq / G_qq) W_latest[l]
+//   W[q] = max(0, P_q)            (nnls.cpp:22, the l = q terms cancelled)
+//
+// and after the evaluation P_q restarts from C_q / G_qq. Q lanes own one row;
+// lane k keeps the sums of columns q = m Q + k. The owner hands P_c to the
+// group (shuffle) L columns before c is due; the L-1 newest terms are added
+// by every lane itself, the last one (W[c-1]) as the only FMA on the serial
+// chain, followed by the clip. Padded and skipped (G_jj <= floor) columns
+// have no incoming terms and restart from their own value, so they stay
+// unchanged. The stop rule (nnls.cpp:31-45, ||W_{s+1}-W_s||_F against the
+// first change, cluster-wide) is decided by one reducer warp per CTA from
+// per-row partials while the row warps run up to D sweeps ahead; each sweep's
+// result is kept in a D-deep shared-memory stash, so the rows just stop and
+// take the stashed result of the deciding sweep.
+// ===========================================================================
+
+constexpr int kStreamTPB = 160;  // up to four row warps + the reducer warp: <= 2 warps per SM sub-partition, 255 registers
+constexpr int kStreamDC = 16;    // cluster exchange ring (slots per CTA): 2 D, see the reducer
+constexpr int kStreamRowLanes = 96;  // target row lanes per CTA (three row warps)
+
+template <int RP, int Q, int L>
+struct StreamShape {
+  static constexpr int PQ = RP / Q;         // owned columns per lane
+  static constexpr int PQ2 = (PQ + 1) / 2;  // as double2
+  static constexpr int WN2 = L / 2;         // window coefficients h_{j,j+1..j+L-1} as double2 (L-1 used)
+  static constexpr int D = 8;               // sweeps in flight (stash depth)
+  static_assert(RP % Q == 0 && L >= 2 && L < RP && (Q == 1 || L >= 3), "stream shape");
+  static_assert((32 / Q) % 4 == 0 || Q == 16, "row slots per warp: a multiple of four (Gram partials)");
+};
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "W_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra W_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+
+// Non-blocking: has the phase with this parity completed? (warp-uniform via lane 0)
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t phase) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(phase)
+      : "memory");
+  return __shfl_sync(0xffffffffu, ok, 0) != 0;
+}
+
+__device__ __forceinline__ unsigned long long ld_volatile_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.volatile.shared.u64 %0, [%1];" : "=l"(v) : "r"(smem_u32(p)) : "memory");
+  return v;
+}
+
+// max(0, v) for okm == -1 (Eigen's cwiseMax, up to the sign of zero), v for
+// okm == 0 (skipped column): sign-bit masking, two integer ops on the chain.
+__device__ __forceinline__ double clip_mask(double v, int okm) {
+#ifndef NTF_NNLS_FCLIP
+  const int hi = __double2hiint(v), lo = __double2loint(v);
+  const int m = (hi >> 31) & okm;
+  return __hiloint2double(hi & ~m, lo & ~m);
+#else
+  return (okm != 0 && v < 0.0) ? 0.0 : v;
+#endif
+}
+
+template <int RP, int Q, int L>
+__global__ void __launch_bounds__(kStreamTPB, 1) nnls_stream_kernel(NnlsLaunch a) {
+  using SS = StreamShape<RP, Q, L>;
+  constexpr int PQ = SS::PQ, PQ2 = SS::PQ2, WN2 = SS::WN2, D = SS::D;
+  constexpr int LDC = RP + 1;
+  extern __shared__ __align__(16) double smem[];
+  cg::cluster_group cl = cg::this_cluster();
+
+  RunState* st = a.st;
+  if (st && st->done) return;  // budget exhausted: the whole iteration is a no-op (uniform)
+  const long long t_begin = clock64();
+
+  const int nrw = int(blockDim.x >> 5) - 1;  // row warps; warp nrw reduces
+  const int nloc = nrw * 32 / Q;              // row slots per CTA
+  const int rpc = (a.rows + int(gridDim.x) - 1) / int(gridDim.x);
+  const unsigned ncta = cl.num_blocks(), me = cl.block_rank();
+
+  double2* pushc = reinterpret_cast<double2*>(smem);  // [RP][PQ2][Q]: h_{j,q}, q = m Q + k (pushed terms)
+  double2* wins = pushc + RP * PQ2 * Q;               // [RP][WN2]: h_{j,j+d}, d = 1..L-1 (window terms)
+  double* Gs = reinterpret_cast<double*>(wins + RP * WN2);  // RP*RP
+  double* Ginv = Gs + RP * RP;                             // RP
+  double* stash = Ginv + RP;                               // [D][RP][nloc]: W after each sweep
+  double* Cs = stash + D * RP * nloc;                      // [nloc][LDC]: rows of C
+  double* stage = Cs + nloc * LDC;                         // [RP][nloc]: extrapolated twin
+  double* part = stage + RP * nloc;                        // 2*RP*RP + 2: Gram partials, <W,C>, quad
+  double* d2part = part + 2 * RP * RP + 2;                 // [D][nloc]: per-row ||dW||^2
+  double* cslot = d2part + D * nloc;                       // [kStreamDC][kMaxCluster]
+  double* red = cslot + kStreamDC * kMaxCluster;           // 32
+  uint64_t* rowbar = reinterpret_cast<uint64_t*>(red + 32);  // D
+  uint64_t* cbar = rowbar + D;                                // kStreamDC
+  unsigned long long* ctl = reinterpret_cast<unsigned long long*>(cbar + kStreamDC);  // (stop << 32) | decided
+
+  const int r = a.rank, mode = a.mode;
+  DevFactors* F = a.F;
+  // pointer chase F -> sel / buffers in one round trip (both buffers' pointers, then select)
+  int selv[kMaxOrder];
+  const double* gp0[kMaxOrder];
+  const double* gp1[kMaxOrder];
+  double* xp0 = nullptr;
+  double* xp1 = nullptr;
+  int sel = 0;
+  if (F) {
+#pragma unroll
+    for (int j = 0; j < kMaxOrder; ++j)
+      if (j < a.order) {
+        selv[j] = F->sel[j];
+        gp0[j] = F->gram[j][0];
+        gp1[j] = F->gram[j][1];
+      }
+    xp0 = F->x[mode][0];
+    xp1 = F->x[mode][1];
+#pragma unroll
+    for (int j = 0; j < kMaxOrder; ++j)
+      if (j == mode) sel = selv[j];
+  }
+  double* X = sel ? xp1 : xp0;
+  const double beta = (a.role == 0) ? st->beta : 0.0;
+  const int max_iters = (a.role == 2) ? a.max_iters : st->inner_max_iters;
+  const double tol = (a.role == 2) ? a.tol : st->tol;
+  const double* w0 = (a.role == 2) ? a.w0 : X;
+  const double* C = a.C;
+
+  // ---- G: Hadamard of the other modes' Grams (kernels.cpp:193-200).
+  // (global loads of four entries per thread in flight together)
+  for (int e0 = threadIdx.x; e0 < RP * RP; e0 += 4 * blockDim.x) {
+    double g[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int e = e0 + u * int(blockDim.x);
+      const int p = e / RP, q = e % RP;
+      g[u] = 0.0;
+      if (e < RP * RP && p < r && q < r) {
+        if (a.role == 2) {
+          g[u] = a.gram_in[p * r + q];
+        } else {
+          g[u] = 1.0;
+#pragma unroll
+          for (int j = 0; j < kMaxOrder; ++j)
+            if (j < a.order && j != mode) g[u] *= (selv[j] ? gp1[j] : gp0[j])[p * r + q];
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (e0 + u * int(blockDim.x) < RP * RP) Gs[e0 + u * int(blockDim.x)] = g[u];
+  }
+  for (int e0 = threadIdx.x; e0 < nloc * RP; e0 += 4 * blockDim.x) {
+    double cv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int e = e0 + u * int(blockDim.x);
+      const int i = e / RP, l = e % RP;
+      const int gr = int(blockIdx.x) * rpc + i;
+      cv[u] = (e < nloc * RP && i < rpc && gr < a.rows && l < r) ? C[(long long)gr * r + l] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int e = e0 + u * int(blockDim.x);
+      if (e < nloc * RP) Cs[(e / RP) * LDC + e % RP] = cv[u];
+    }
+  }
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < D; ++b)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&rowbar[b])) : "memory");
+    for (int b = 0; b < kStreamDC; ++b)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&cbar[b])) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    *ctl = 0ull;
+  }
+  __syncthreads();
+  const long long t_p1 = clock64();
+  double dmax = -INFINITY;
+  for (int j = 0; j < r; ++j) dmax = fmax(dmax, Gs[j * RP + j]);
+  const double diag_floor = 1e-12 * dmax;  // nnls.cpp:16-19
+  unsigned okbits = 0;                      // columns that are updated (and clipped)
+  for (int j = 0; j < r; ++j)
+    if (Gs[j * RP + j] > diag_floor) okbits |= 1u << j;
+  for (int j = threadIdx.x; j < RP; j += blockDim.x) Ginv[j] = ((okbits >> j) & 1) ? 1.0 / Gs[j * RP + j] : 0.0;
+  __syncthreads();
+  {
+    double* pc = reinterpret_cast<double*>(pushc);
+    for (int e = threadIdx.x; e < RP * PQ2 * Q * 2; e += blockDim.x) {
+      const int j = e / (PQ2 * Q * 2), rem = e % (PQ2 * Q * 2);
+      const int m2 = rem / (Q * 2), k = (rem / 2) % Q, half = rem & 1;
+      const int m = 2 * m2 + half, q = m * Q + k;
+      double h = 0.0;
+      if (m < PQ && q < r && j < r && q != j && ((q - j + RP) % RP) >= L && ((okbits >> q) & 1))
+        h = Gs[j * RP + q] * Ginv[q];
+      pc[e] = h;
+    }
+    double* wn = reinterpret_cast<double*>(wins);
+    for (int e = threadIdx.x; e < RP * WN2 * 2; e += blockDim.x) {
+      const int j = e / (WN2 * 2), d = e % (WN2 * 2) + 1, c = (j + d) % RP;
+      double h = 0.0;
+      if (d <= L - 1 && j < r && c < r && ((okbits >> c) & 1)) h = Gs[j * RP + c] * Ginv[c];
+      wn[e] = h;
+    }
+  }
+  const long long t_p2 = clock64();
+  cl.sync();  // tables, C rows and every CTA's mbarriers exist before any st.async targets them
+  const long long t_loop = clock64();
+
+  const int warp = int(threadIdx.x >> 5), lane = int(threadIdx.x & 31);
+  if (warp < nrw) {
+    // ------------------------------------------------------------ row warps
+    const int slot = (warp * 32 + lane) / Q, k = lane % Q, gbase = lane & ~(Q - 1);
+    const int row = int(blockIdx.x) * rpc + slot;
+    const bool valid = slot < rpc && row < a.rows;
+    double Wl[RP];  // latest value of every column of the row (all lanes of the group)
+#pragma unroll
+    for (int l = 0; l < RP; ++l) Wl[l] = (valid && l < r) ? w0[(long long)row * r + l] : 0.0;
+    const double* pcd = reinterpret_cast<const double*>(pushc);
+    // restart values and pending sums of the owned columns (as if the
+    // previous sweep had pushed W0[l > q]; W0[l < q] arrive in sweep 0)
+    double rv[PQ], P[PQ];
+#pragma unroll
+    for (int m = 0; m < PQ; ++m) {
+      const int q = m * Q + k;
+      double v = 0.0;
+      if (q < r) v = ((okbits >> q) & 1) ? Cs[slot * LDC + q] * Ginv[q] : (valid ? w0[(long long)row * r + q] : 0.0);
+      rv[m] = v;
+      double pm = v;
+#pragma unroll
+      for (int j = 0; j < RP; ++j)
+        if (j > q) pm = fma(-Wl[j], pcd[((j * PQ2 + m / 2) * Q + k) * 2 + (m & 1)], pm);
+      P[m] = pm;
+    }
+    auto bcast = [&](double v, int c) -> double {
+      if constexpr (Q > 1)
+        return __shfl_sync(0xffffffffu, v, gbase | (c % Q));
+      else
+        return v;
+    };
+    auto win = [&](int j, int d) -> double {  // h_{j, j+d}
+      return reinterpret_cast<const double*>(wins)[j * WN2 * 2 + d - 1];
+    };
+    double acc[RP];  // per column: its handed-over sum plus the window terms so far
+#pragma unroll
+    for (int c = 0; c < L; ++c) {
+      acc[c] = bcast(P[c / Q], c);
+#pragma unroll
+      for (int d = L - 1; d >= 2; --d)
+        if (d > c) acc[c] = fma(-win((c - d + RP) % RP, d), Wl[(c - d + RP) % RP], acc[c]);
+    }
+    // coefficient registers of the next two steps (rows j of pushc / wins)
+    double2 pcr[RP][PQ2], wr[RP][WN2];
+    auto load_row = [&](int j) {
+#pragma unroll
+      for (int m2 = 0; m2 < PQ2; ++m2) pcr[j][m2] = pushc[(j * PQ2 + m2) * Q + k];
+#pragma unroll
+      for (int w = 0; w < WN2; ++w) wr[j][w] = wins[j * WN2 + w];
+    };
+    load_row(RP - 1);
+    load_row(0);
+    load_row(1);
+    auto wcoef = [&](int j, int d) -> double {  // h_{j,j+d} from the registers
+      const double2 x = wr[j][(d - 1) / 2];
+      return ((d - 1) & 1) ? x.y : x.x;
+    };
+    auto pcoef = [&](int j, int m) -> double {
+      const double2 x = pcr[j][m / 2];
+      return (m & 1) ? x.y : x.x;
+    };
+
+    // sweep s's result is stashed during sweep s + 1 (each column just before
+    // it is overwritten) or on leaving the loop; the per-row change goes to
+    // the reducer with st.async (completes bytes on rowbar, no fence)
+    const uint32_t d2addr = smem_u32(d2part + slot);
+    int s = 0;
+    long long passes = 0, pass_cyc = 0;
+    unsigned long long c = ld_volatile_u64(ctl);
+    for (;;) {
+      if (c >> 32) break;
+      if (s >= max_iters || (s >= D && int(c & 0xffffffffu) < s - D + 1)) {
+        do {
+          __nanosleep(20);
+          c = ld_volatile_u64(ctl);
+        } while (!(c >> 32) && (s >= max_iters || int(c & 0xffffffffu) < s - D + 1));
+        if (c >> 32) break;
+      }
+      double d2 = 0.0;
+      double* stp = stash + ((s + D - 1) % D) * RP * nloc + slot;  // slot of sweep s - 1
+      const long long tp0 = pclock();
+#pragma unroll
+      for (int j = 0; j < RP; ++j) {
+        const int jm1 = (j + RP - 1) % RP;
+        const double v = fma(-wcoef(jm1, 1), Wl[jm1], acc[j]);
+        const double nw = clip_mask(v, -int((okbits >> j) & 1u));
+        if (k == 0) stp[j * nloc] = Wl[j];
+        const double dd = nw - Wl[j];
+        d2 = fma(dd, dd, d2);
+        Wl[j] = nw;
+#pragma unroll
+        for (int d = 2; d < L; ++d) acc[(j + d) % RP] = fma(-wcoef(j, d), nw, acc[(j + d) % RP]);
+#pragma unroll
+        for (int m = 0; m < PQ; ++m) P[m] = fma(-nw, pcoef(j, m), P[m]);
+        if (k == j % Q) P[j / Q] = rv[j / Q];
+        acc[(j + L) % RP] = bcast(P[((j + L) % RP) / Q], (j + L) % RP);
+        load_row((j + 2) % RP);
+        if (j == RP / 2) c = ld_volatile_u64(ctl);  // decisions so far, checked after the pass
+      }
+      pass_cyc += pclock() - tp0;
+      if (k == 0) {
+        const int b = s % D;
+        asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(
+                         d2addr + uint32_t(b * nloc * 8)),
+                     "l"(__double_as_longlong(d2)), "r"(smem_u32(&rowbar[b]))
+                     : "memory");
+      }
+      ++s;
+      ++passes;
+    }
+    if (k == 0) {  // the last sweep's result (or W0 when no sweep ran)
+      double* stp = stash + ((s + D - 1) % D) * RP * nloc + slot;
+#pragma unroll
+      for (int l = 0; l < RP; ++l) stp[l * nloc] = Wl[l];
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      g_nnls_prof[5] += passes;
+      g_nnls_prof[6] += pass_cyc;
+    }
+  } else {
+    // -------------------------------------------------------- reducer warp
+    // Two decoupled stages over the sweeps, in order: post (this CTA's rows
+    // are done with sweep np: sum their partials, send the sum to every CTA)
+    // and decide (every CTA's sum of sweep nd has arrived: add them in rank
+    // order -- the same bits in every CTA -- and apply the stop rule). Posts
+    // run ahead of decisions, so the cluster latency overlaps the sweeps.
+    double first = 0.0;
+    if (max_iters <= 0) {
+      if (lane == 0) asm volatile("st.volatile.shared.u64 [%0], %1;" ::"r"(smem_u32(ctl)), "l"(1ull << 32) : "memory");
+    } else {
+      int np = 0, nd = 0;
+      if (lane == 0)
+        for (int b = 0; b < D; ++b)
+          asm volatile("mbarrier.arrive.expect_tx.relaxed.cta.shared::cta.b64 _, [%0], %1;" ::"r"(
+                           smem_u32(&rowbar[b])),
+                       "r"(unsigned(nloc) * 8u)
+                       : "memory");
+      for (;;) {
+        bool idle = true;
+        if (np < max_iters && mbar_test(&rowbar[np % D], uint32_t(np / D) & 1u)) {
+          const int b = np % D;
+          double x = 0.0;
+          for (int i = lane; i < nloc; i += 32) x += d2part[b * nloc + i];
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+          const int cb = np % kStreamDC;
+          if (lane == 0)
+            asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(
+                             smem_u32(&cbar[cb])),
+                         "r"(ncta * 8u)
+                         : "memory");
+          if (unsigned(lane) < ncta) {
+            uint32_t raddr, rbar;
+            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
+                         : "=r"(raddr)
+                         : "r"(smem_u32(&cslot[cb * kMaxCluster + me])), "r"(lane));
+            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rbar) : "r"(smem_u32(&cbar[cb])), "r"(lane));
+            asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(raddr),
+                         "l"(__double_as_longlong(x)), "r"(rbar)
+                         : "memory");
+          }
+          if (lane == 0)  // re-arm this barrier for sweep np + D
+            asm volatile("mbarrier.arrive.expect_tx.relaxed.cta.shared::cta.b64 _, [%0], %1;" ::"r"(
+                             smem_u32(&rowbar[b])),
+                         "r"(unsigned(nloc) * 8u)
+                         : "memory");
+          ++np;
+          idle = false;
+        }
+        if (nd < np && mbar_test(&cbar[nd % kStreamDC], uint32_t(nd / kStreamDC) & 1u)) {
+          const int cb = nd % kStreamDC;
+          double ch2 = 0.0;  // ||W_{s+1} - W_s||_F^2, CTAs in rank order: same bits everywhere
+          for (unsigned c = 0; c < ncta; ++c) ch2 += cslot[cb * kMaxCluster + c];
+          if (nd == 0) first = sqrt(ch2);
+          const bool stop = (nd + 1 >= max_iters) || stop_rule(ch2, tol * first);
+          if (lane == 0) {
+            const unsigned long long w = (stop ? (1ull << 32) : 0ull) | unsigned(nd + 1);
+            asm volatile("st.volatile.shared.u64 [%0], %1;" ::"r"(smem_u32(ctl)), "l"(w) : "memory");
+          }
+          if (stop) break;
+          ++nd;
+          idle = false;
+        }
+        if (idle) __nanosleep(64);
+      }
+    }
+  }
+  __syncthreads();
+  const long long t_loop_end = clock64();
+  const int s = int(*ctl & 0xffffffffu);  // sweeps run (nnls.cpp:31-45)
+  const int fs = (s + D - 1) % D;         // stash slot of the result
+
+  if (a.role == 2) {
+    for (int e = threadIdx.x; e < nloc * RP; e += blockDim.x) {
+      const int i = e / RP, l = e % RP;
+      const int row = int(blockIdx.x) * rpc + i;
+      if (i < rpc && row < a.rows && l < r) a.w_out[(long long)row * r + l] = stash[(fs * RP + l) * nloc + i];
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0 && a.sweeps_out) *a.sweeps_out = s;
+    cl.sync();  // no CTA leaves while cluster traffic may target it
+    return;
+  }
+
+  // ---- write the block (HER: solved + extrapolated twin; AO: in place).
+  const double* Wf = stash + fs * RP * nloc;  // [RP][nloc]
+  double* S = F->x[mode][sel ^ 1];
+  float* X32 = F->x32[mode][sel];
+  float* S32 = F->x32[mode][sel ^ 1];
+  for (int e0 = threadIdx.x; e0 < nloc * RP; e0 += 4 * blockDim.x) {
+    double old[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {  // the accepted block's values, loads in flight together
+      const int e = e0 + u * int(blockDim.x);
+      const int i = e / RP, l = e % RP;
+      const int row = int(blockIdx.x) * rpc + i;
+      old[u] = (a.role == 0 && e < nloc * RP && i < rpc && row < a.rows && l < r) ? X[(long long)row * r + l] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int e = e0 + u * int(blockDim.x);
+      if (e >= nloc * RP) break;
+      const int i = e / RP, l = e % RP;
+      const int row = int(blockIdx.x) * rpc + i;
+      const double w = Wf[l * nloc + i];
+      double h = 0.0;
+      if (i < rpc && row < a.rows && l < r) {
+        const long long o = (long long)row * r + l;
+        if (a.role == 0) {
+          h = clip0(__dadd_rn(w, __dmul_rn(beta, __dsub_rn(w, old[u]))));  // her.cpp:16-19
+          S[o] = w;
+          if (S32) S32[o] = float(w);
+        } else {
+          h = w;
+        }
+        X[o] = h;
+        if (X32) X32[o] = float(h);
+      }
+      if (a.role == 0) stage[l * nloc + i] = h;
+    }
+  }
+  __syncthreads();
+  const long long t_e1 = clock64();
+  // ---- Gram partials of this CTA's rows (W, and the twin for HER)
+  for (int e = threadIdx.x; e < RP * RP; e += blockDim.x) {
+    const int p = e / RP, q = e % RP;
+    if (p > q || q >= r) continue;
+    // four rows per step, two accumulator pairs per matrix (nloc % 4 == 0)
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0, h0 = 0.0, h1 = 0.0, h2 = 0.0, h3 = 0.0;
+    const double2* wp = reinterpret_cast<const double2*>(Wf + p * nloc);
+    const double2* wq = reinterpret_cast<const double2*>(Wf + q * nloc);
+    const double2* hp = reinterpret_cast<const double2*>(stage + p * nloc);
+    const double2* hq = reinterpret_cast<const double2*>(stage + q * nloc);
+    const bool twin = a.role == 0;
+    for (int i = 0; i < nloc / 2; i += 2) {
+      const double2 a0 = wp[i], a1 = wp[i + 1], b0 = wq[i], b1 = wq[i + 1];
+      s0 = fma(a0.x, b0.x, s0);
+      s1 = fma(a0.y, b0.y, s1);
+      s2 = fma(a1.x, b1.x, s2);
+      s3 = fma(a1.y, b1.y, s3);
+      if (twin) {
+        const double2 c0 = hp[i], c1 = hp[i + 1], d0 = hq[i], d1 = hq[i + 1];
+        h0 = fma(c0.x, d0.x, h0);
+        h1 = fma(c0.y, d0.y, h1);
+        h2 = fma(c1.x, d1.x, h2);
+        h3 = fma(c1.y, d1.y, h3);
+      }
+    }
+    part[e] = (s0 + s1) + (s2 + s3);
+    if (twin) part[RP * RP + e] = (h0 + h1) + (h2 + h3);
+  }
+  if (a.last) {
+    // <W, C> and <W^T W, G> of this CTA (the cheap objective's data terms)
+    __syncthreads();
+    double cr = 0.0, qd = 0.0;
+    for (int e = threadIdx.x; e < nloc * RP; e += blockDim.x) {
+      const int i = e / RP, l = e % RP;
+      if (l < r) cr += Wf[l * nloc + i] * Cs[i * LDC + l];
+    }
+    for (int e = threadIdx.x; e < RP * RP; e += blockDim.x) {
+      const int p = e / RP, q = e % RP;
+      if (p < r && q < r) qd += part[p <= q ? p * RP + q : q * RP + p] * Gs[e];
+    }
+    cr = block_sum(cr, red);
+    qd = block_sum(qd, red);
+    if (threadIdx.x == 0) {
+      part[2 * RP * RP] = cr;
+      part[2 * RP * RP + 1] = qd;
+    }
+  }
+  const long long t_e2 = clock64();
+  cl.sync();  // partials visible cluster-wide
+  const long long t_e3 = clock64();
+  double* gW = (a.role == 0) ? F->gram[mode][sel ^ 1] : F->gram[mode][sel];
+  double* gH = F->gram[mode][sel];
+  const int nmat = (a.role == 0) ? 2 : 1;
+  for (int e = int(threadIdx.x) * int(ncta) + int(me); e < nmat * RP * RP; e += int(blockDim.x) * int(ncta)) {
+    const int mat = e / (RP * RP), pq = e % (RP * RP);
+    const int p = pq / RP, q = pq % RP;
+    if (p > q || q >= r) continue;
+    double vals[kMaxCluster];
+#pragma unroll
+    for (int c = 0; c < kMaxCluster; ++c) vals[c] = c < int(ncta) ? cl.map_shared_rank(part, unsigned(c))[e] : 0.0;
+    double v = 0.0;
+#pragma unroll
+    for (int c = 0; c < kMaxCluster; ++c)
+      if (c < int(ncta)) v += vals[c];
+    double* dst = mat ? gH : gW;
+    dst[p * r + q] = v;
+    dst[q * r + p] = v;
+  }
+  double cross = 0.0, quad = 0.0;
+  if (a.last && blockIdx.x == 0 && threadIdx.x == 0) {
+    double cv[kMaxCluster], qv[kMaxCluster];  // all remote loads in flight before the ordered sums
+#pragma unroll
+    for (int c = 0; c < kMaxCluster; ++c) {
+      const double* pc = cl.map_shared_rank(part, unsigned(c < int(ncta) ? c : 0));
+      cv[c] = c < int(ncta) ? pc[2 * RP * RP] : 0.0;
+      qv[c] = c < int(ncta) ? pc[2 * RP * RP + 1] : 0.0;
+    }
+#pragma unroll
+    for (int c = 0; c < kMaxCluster; ++c)
+      if (c < int(ncta)) {
+        cross += cv[c];
+        quad += qv[c];
+      }
+  }
+  const long long t_e4 = clock64();
+  cl.sync();  // remote reads done before any CTA exits
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    const long long t_end = clock64();
+    unsigned long long* ph = &g_nnls_skew[2][64];  // phase cycles (diagnostics)
+    ph[0] += t_p1 - t_begin;
+    ph[1] += t_p2 - t_p1;
+    ph[2] += t_loop - t_p2;
+    ph[3] += t_e1 - t_loop_end;
+    ph[4] += t_e2 - t_e1;
+    ph[5] += t_e3 - t_e2;
+    ph[6] += t_e4 - t_e3;
+    ph[7] += t_end - t_e4;
+    g_nnls_prof[0] += t_loop_end - t_loop;
+    g_nnls_prof[1] += t_loop - t_begin;
+    g_nnls_prof[2] += s;
+    g_nnls_prof[3] += 1;
+    g_nnls_prof[4] += t_end - t_loop_end;
+  }
+  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  if (!a.last) {
+    st->last_sweeps[mode] = s;
+    return;
+  }
+  const double f = 0.5 * st->nsq - cross + 0.5 * quad;
+  st->last_sweeps[mode] = s;
+  const int kk = st->k + 1;
+  const double time_s = double(globaltimer() - st->t_start_ns) * 1e-9;
+  TraceEntry rec;
+  rec.f = f;
+  rec.time_s = time_s;
+  rec.sweeps = 0;
+  for (int j = 0; j < a.order; ++j) rec.sweeps += st->last_sweeps[j];
+  if (a.role == 0) {
+    const bool restarted = f > st->f_prev;  // strict (her.cpp:75)
+    if (restarted)
+      for (int j = 0; j < a.order; ++j) F->sel[j] ^= 1;  // X := S for every mode
+    st->f_prev = f;                                      // even on rejection (:84)
+    rec.beta = st->beta;                                 // beta_used
+    rec.restarted = restarted ? 1 : 0;
+    if (restarted) {  // update_betas (her.cpp:21-30)
+      st->beta_bar = st->beta;
+      st->beta = __ddiv_rn(st->beta, st->eta);
+    } else {
+      st->beta = fmin(st->beta_bar, __dmul_rn(st->beta, st->gamma));
+      st->beta_bar = fmin(1.0, __dmul_rn(st->beta_bar, st->gamma_bar));
+    }
+  } else {
+    rec.beta = 0.0;
+    rec.restarted = 0;
+  }
+  a.trace[kk - 1] = rec;
+  st->f_last = f;
+  st->k = kk;
+  if ((st->max_iters > 0 && kk >= st->max_iters) || (st->max_time_s > 0.0 && time_s >= st->max_time_s))
+    st->done = 1;
+}
+
+template <int RP, int Q, int L>
+bool launch_stream_q(const NnlsLaunch& a, cudaStream_t s) {
+  using SS = StreamShape<RP, Q, L>;
+  const long long lanes = (long long)a.rows * Q;
+  const int cl = int(std::max(1LL, std::min<long long>((lanes + kStreamRowLanes - 1) / kStreamRowLanes, kMaxCluster)));
+  const int rpc = (a.rows + cl - 1) / cl;
+  const int roww = (rpc * Q + 31) / 32;
+  const int threads = (roww + 1) * 32;
+  if (threads > kStreamTPB) return false;
+  const size_t nloc = size_t(roww) * 32 / Q;
+  const size_t smem = sizeof(double2) * (RP * SS::PQ2 * Q + RP * SS::WN2) +
+                      sizeof(double) * (RP * RP + RP + SS::D * RP * nloc + nloc * (RP + 1) + RP * nloc +
+                                        2 * RP * RP + 2 + SS::D * nloc + kStreamDC * kMaxCluster + 32) +
+                      sizeof(uint64_t) * (SS::D + kStreamDC + 1);
+  auto fn = nnls_stream_kernel<RP, Q, L>;
+  NTF_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  if (cl > 8) NTF_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  NnlsLaunch args = a;
+  void* params[] = {&args};
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(cl);
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cl;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  NTF_CUDA(cudaLaunchKernelExC(&cfg, reinterpret_cast<const void*>(fn), params));
+  return true;
+}
+
+// Lane split by padded rank: about four owned columns per lane, narrower
+// groups for factors too tall for the cluster.
+template <int RP, int Q0>
+bool launch_stream_rp(const NnlsLaunch& a, cudaStream_t s) {
+  if constexpr (Q0 > 1) {
+    if (launch_stream_q<RP, Q0, 4>(a, s)) return true;
+    return launch_stream_rp<RP, Q0 / 2>(a, s);
+  } else {
+    return launch_stream_q<RP, 1, 2>(a, s);
+  }
+}
+
+bool launch_stream(const NnlsLaunch& a, cudaStream_t s) {
+  static const bool off = [] {
+    const char* e = std::getenv("NTF_NNLS_OLD");
+    return e && std::atoi(e) != 0;
+  }();
+  if (off) return false;
+  const int r = a.rank;
+  if (r <= 4) return launch_stream_rp<4, 1>(a, s);
+  if (r <= 8) return launch_stream_rp<8, 2>(a, s);
+  if (r <= 10) return launch_stream_rp<10, 2>(a, s);
+  if (r <= 12) return launch_stream_rp<12, 4>(a, s);
+  if (r <= 16) return launch_stream_rp<16, 4>(a, s);
+  if (r <= 20) return launch_stream_rp<20, 4>(a, s);
+  if (r <= 24) return launch_stream_rp<24, 8>(a, s);
+  if (r <= 32) return launch_stream_rp<32, 8>(a, s);
+  return false;
+}
+
 }  // namespace
 
 void nnls_prof_read(unsigned long long out[8 + 384], bool reset) {
@@ -665,6 +1334,7 @@ void nnls_prof_read(unsigned long long out[8 + 384], bool reset) {
 void launch_nnls(const NnlsLaunch& a, cudaStream_t s) {
   const int r = a.rank;
   if (r < 1 || r > kMaxRank) throw Unsupported("rank outside the fused NNLS kernel's range (1..64)");
+  if (launch_stream(a, s)) return;
   if (a.rows > kMaxCluster * 256) throw Unsupported("factor taller than 4096 rows");
   if (r <= 4) return launch_rp<4, 256>(a, s);
   if (r <= 8) return launch_rp<8, 256>(a, s);

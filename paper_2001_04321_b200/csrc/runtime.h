@@ -20,7 +20,7 @@ namespace ntfb {
 uint64_t stream_seed(uint64_t base, uint64_t stream);
 void random_init(const int* shape, int order, int rank, uint64_t seed, double* out);
 void generate(const int* shape, int order, int rank, double sigma, int ill, int collinear, uint64_t seed,
-              int dtype, void* tensor, double* truth);
+              int dtype, void* tensor, double* truth, long long slab_b = -1, long long slab_e = -1);
 double factor_error(const double* est, const double* truth, const int* shape, int order, int rank);
 
 // ---- device memory ------------------------------------------------------------

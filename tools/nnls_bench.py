@@ -29,3 +29,13 @@ def t(iters, reps=30):
 t1, t50 = t(1), t(50)
 print(f"nnls rows={rows} r={r} Q={os.environ.get('NTF_NNLS_Q', 'auto')}: 1 sweep {t1*1e6:.1f} us, 50 sweeps {t50*1e6:.1f} us,"
       f" per sweep {(t50 - t1) / 49 * 1e6:.2f} us = {(t50 - t1) / 49 * 1.965e9:.0f} cycles")
+
+import ctypes as _C
+from paper_2001_04321_b200 import _lib as _L
+_buf = (_C.c_ulonglong * (8 + 384))()
+_L.lib().ntf_debug_nnls_prof(_buf, 1)
+t(50, reps=10)
+if _L.lib().ntf_debug_nnls_prof(_buf, 1) == 0 and _buf[3]:
+    loop, red, sw, calls, pc, npass, tri, _ = list(_buf)[:8]
+    print(f"  CTA0: {loop / calls:.0f} cyc/call, {sw / calls:.1f} sweeps/call, {loop / max(sw, 1):.0f} cyc/sweep, "
+          f"reduction {red / max(sw, 1):.0f}, pass {pc / max(npass, 1):.0f} (triangle {tri / max(npass, 1):.0f})")

@@ -42,6 +42,14 @@ if _L.lib().ntf_debug_nnls_prof(_buf, 1) == 0 and _buf[3]:
         p0 = min(post[i] for i in idx)
         print("  pass-4 per warp (ns from first post): post / fin start / fin end")
         print("   " + " ".join(f"{post[i]-p0}/{fs[i]-p0}/{fin[i]-p0}" for i in idx[:24]))
-    print(f"  nnls CTA0: {loop / calls:.0f} cyc/call, {sw / calls:.1f} sweeps/call, "
-          f"{loop / max(sw, 1):.0f} cyc/sweep of which reduction {red / max(sw, 1):.0f}; "
-          f"pass {pc / max(npass, 1):.0f} cyc (triangle {tri / max(npass, 1):.0f}), {npass / calls:.1f} passes/call")
+    if os.environ.get("NTF_NNLS_OLD"):
+        print(f"  nnls CTA0: {loop / calls:.0f} cyc/call, {sw / calls:.1f} sweeps/call, "
+              f"{loop / max(sw, 1):.0f} cyc/sweep of which reduction {red / max(sw, 1):.0f}; "
+              f"pass {pc / max(npass, 1):.0f} cyc (triangle {tri / max(npass, 1):.0f}), {npass / calls:.1f} passes/call")
+    else:  # stream kernel: [0] loop, [1] prologue, [4] epilogue, [5] passes, [6] pass cycles (profile builds)
+        print(f"  nnls (stream) CTA0 per call: prologue {red / calls:.0f} cyc, loop {loop / calls:.0f} cyc "
+              f"({sw / calls:.1f} sweeps, {npass / calls:.1f} passes, {loop / max(sw, 1):.0f} cyc/sweep, "
+              f"pass {tri / max(npass, 1):.0f} cyc), epilogue {pc / calls:.0f} cyc")
+        ph = b[8 + 256 + 64: 8 + 256 + 72]
+        print("  phases/call: G+C loads %.0f | tables %.0f | cl.sync %.0f || writes %.0f | gram part %.0f | cl.sync %.0f | reduce %.0f | cl.sync+ %.0f"
+              % tuple(x / calls for x in ph))
