@@ -333,6 +333,18 @@ void fast_mttkrp(const void* t, int dtype, const ModeView& v, const DevFactors* 
     fprintf(stderr, "[fast-prof mode %d] CTA starts spread %.1f us, ends spread %.1f us, avg CTA span %.1f us, "
             "first start to last end %.1f us\n", v.mode, (gs0 - g0) * 1e-3, (g1 - gs1) * 1e-3, gspan * 1e-3,
             (g1 - g0) * 1e-3);
+    double ep[3] = {0, 0, 0};
+    unsigned long long gend = 0;
+    for (int b = 0; b < ch.grid; ++b) {
+      const unsigned long long* q = &h[size_t(b) * fast::kProfSlots];
+      if (q[8]) ep[0] += double(q[8] - q[7]) / ch.grid;
+      if (q[9]) ep[1] += double(q[9] - q[8]) / ch.grid;
+      if (q[10]) ep[2] += double(q[10] - q[9]) / ch.grid;
+      gend = std::max(gend, std::max(q[8], q[10]));
+    }
+    fprintf(stderr, "[fast-prof mode %d] epilogue: fold+partials %.1f us, grid barrier %.1f us, slab reduce %.1f us; "
+            "first start to last epilogue end %.1f us\n", v.mode, ep[0] * 1e-3, ep[1] * 1e-3, ep[2] * 1e-3,
+            (gend - g0) * 1e-3);
     fprintf(stderr,
             "[fast-prof mode %d] units/CTA %.1f | producer %.0f cyc (stage wait %.0f, copy wait %.0f) | "
             "consumer %.0f cyc (data wait %.0f) | %.0f cyc/unit\n",

@@ -362,22 +362,26 @@ __global__ void __launch_bounds__(max_threads_es(A, B, int(sizeof(T))), 1) mttkr
           // Shared-memory bandwidth (128 B/clk/SM, every lane receiving its
           // 16 or 8 bytes even on a broadcast) is the budget: per k a lane
           // reads B W values and A T values for A*B FMAs, so A and B are
-          // large and the register-heavy tile streams one k at a time.
+          // large. A lane's 16-byte chunk of a row holds all VEC k of the
+          // chunk: one read per row, then VEC rank-1 updates.
+          T w[VEC][BP];
 #pragma unroll
-          for (int kk = 0; kk < VEC; ++kk) {
-            T w[BP];
+          for (int kk = 0; kk < VEC; ++kk)
 #pragma unroll
             for (int q = 0; q < NV; ++q) {
               const V x = *reinterpret_cast<const V*>(ws + (pc * VEC + kk) * p.wld + q * VEC);
 #pragma unroll
-              for (int e = 0; e < VEC; ++e) w[q * VEC + e] = VT::get(x, e);
+              for (int e = 0; e < VEC; ++e) w[kk][q * VEC + e] = VT::get(x, e);
             }
 #pragma unroll
-            for (int i = 0; i < A; ++i) {
-              const int m = off[i];
-              const T t = *reinterpret_cast<const T*>(ts + m * 128 + (((pc ^ m) & 7) << 4) + kk * int(sizeof(T)));
+          for (int i = 0; i < A; ++i) {
+            const int m = off[i];
+            const V tv = *reinterpret_cast<const V*>(ts + m * 128 + (((pc ^ m) & 7) << 4));
 #pragma unroll
-              for (int b = 0; b < B; ++b) acc[i][b] = fma(t, w[b], acc[i][b]);
+            for (int kk = 0; kk < VEC; ++kk) {
+              const T t = VT::get(tv, kk);
+#pragma unroll
+              for (int b = 0; b < B; ++b) acc[i][b] = fma(t, w[kk][b], acc[i][b]);
             }
           }
         }
@@ -466,6 +470,14 @@ __global__ void __launch_bounds__(max_threads_es(A, B, int(sizeof(T))), 1) mttkr
         }
       }
     }
+    auto gstamp = [&](int slot) {
+      if (prof_on && cw == 0 && lane == 0) {
+        unsigned long long g;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+        p.prof[blockIdx.x * kProfSlots + slot] = g;
+      }
+    };
+    gstamp(8);
     if (p.counter) {
       // ---------------------------------------------- slab reduction
       // arrive once every slab row of this CTA is written; wait for all CTAs
@@ -489,23 +501,42 @@ __global__ void __launch_bounds__(max_threads_es(A, B, int(sizeof(T))), 1) mttkr
         }
       }
       asm volatile("bar.sync 1, %0;" ::"r"(n_consumers * 32) : "memory");
+      gstamp(9);
+      // Eight lanes per output element: lane t of the octet adds slabs
+      // t, t + 8, ... in order with all its loads in flight, then the octet
+      // folds (xor 1, 2, 4). The order depends only on the slab count, so
+      // the result is bit-reproducible; every lane of the CTA takes part.
       const long long n = v.I * r;
       const long long per = (n + gridDim.x - 1) / gridDim.x;
       const long long e0 = (long long)blockIdx.x * per;
       const long long e1 = e0 + per < n ? e0 + per : n;
       const int nsl = p.ctas_per_mtile;
-      for (long long e = e0 + (long long)cw * 32 + lane; e < e1; e += (long long)n_consumers * 32) {
+      const int oct = (cw * 32 + lane) >> 3, t8 = lane & 7;
+      const int n_oct = n_consumers * 4;
+      for (long long eb = e0; eb < e1; eb += n_oct) {
+        const long long e = eb + oct;
+        const bool ok = e < e1;
         double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-        int q = 0;
-        for (; q + 4 <= nsl; q += 4) {
-          s0 += __ldcg(p.partial + (size_t(q) * n + e));
-          s1 += __ldcg(p.partial + (size_t(q + 1) * n + e));
-          s2 += __ldcg(p.partial + (size_t(q + 2) * n + e));
-          s3 += __ldcg(p.partial + (size_t(q + 3) * n + e));
+        int q = t8;
+#pragma unroll 4
+        for (; q + 24 < nsl; q += 32) {
+          const double x0 = ok ? __ldcg(p.partial + (size_t(q) * n + e)) : 0.0;
+          const double x1 = ok ? __ldcg(p.partial + (size_t(q + 8) * n + e)) : 0.0;
+          const double x2 = ok ? __ldcg(p.partial + (size_t(q + 16) * n + e)) : 0.0;
+          const double x3 = ok ? __ldcg(p.partial + (size_t(q + 24) * n + e)) : 0.0;
+          s0 += x0;
+          s1 += x1;
+          s2 += x2;
+          s3 += x3;
         }
-        for (; q < nsl; ++q) s0 += __ldcg(p.partial + (size_t(q) * n + e));
-        p.out[e] = (s0 + s1) + (s2 + s3);
+        for (; q < nsl; q += 8) s0 += ok ? __ldcg(p.partial + (size_t(q) * n + e)) : 0.0;
+        double sum = (s0 + s1) + (s2 + s3);
+        sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+        sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+        sum += __shfl_xor_sync(0xffffffffu, sum, 4);
+        if (ok && t8 == 0) p.out[e] = sum;
       }
+      gstamp(10);
     }
   }
 }

@@ -25,7 +25,7 @@ constexpr int kUnitInts = 6 + 2 * kMaxBase;
 // [2] producer waiting for its copies, [3] consumer total, [4] consumer
 // waiting for a full stage, [5] units, [6] globaltimer at kernel start,
 // [7] globaltimer at the end of the consumer loop
-constexpr int kProfSlots = 8;
+constexpr int kProfSlots = 12;
 
 struct Params {
   ModeView v;
