@@ -688,16 +688,6 @@ struct StreamShape {
   static_assert((32 / Q) % 4 == 0 || Q == 16, "row slots per warp: a multiple of four (Gram partials)");
 };
 
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n"
-      "W_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra W_%=;\n}\n" ::"r"(smem_u32(bar)),
-      "r"(phase)
-      : "memory");
-}
-
 // Non-blocking: has the phase with this parity completed? (warp-uniform via lane 0)
 __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t phase) {
   uint32_t ok;

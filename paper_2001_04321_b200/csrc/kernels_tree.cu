@@ -151,7 +151,9 @@ int tree_chunks(const TreeView& v, int sms) {
   const long long tiles = (pairs + kTreeTile - 1) / kTreeTile;
   const long long Q = v.L * v.R;
   long long chunks = (2LL * sms + tiles - 1) / tiles;
-  chunks = std::max(1LL, std::min(chunks, Q));
+  // a chunk's Khatri-Rao rows live in shared memory (<= 192 KB)
+  const long long min_chunks = (Q * v.rank * (long long)sizeof(double) + 192 * 1024 - 1) / (192 * 1024);
+  chunks = std::max(1LL, std::min(std::max(chunks, min_chunks), Q));
   return int(chunks);
 }
 

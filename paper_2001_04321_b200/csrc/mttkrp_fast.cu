@@ -303,6 +303,14 @@ void fast_mttkrp(const void* t, int dtype, const ModeView& v, const DevFactors* 
   if (!direct && counter && !std::getenv("NTF_FAST_SEPARATE_REDUCE")) ch.p.counter = counter;
   ch.p.utab = unit_table;
   fill_params_modes(v, ch.layout, ch.p);
+  // FP32 register sums over more than ~16k terms drift past the 1e-5
+  // relative bar at BASELINE config 5 (1.05e-5 measured at 2000^3, r = 64)
+  ch.p.flush_units = 0;
+  if (dtype == NTF_DTYPE_F32 && ch.p.KW == 1) {
+    const long long per_cta = (ch.p.units + ch.p.ctas_per_mtile - 1) / ch.p.ctas_per_mtile;
+    const int fu = std::max(1, 16384 / ch.p.kbox);
+    if (per_cta > fu) ch.p.flush_units = fu;
+  }
   // diagnostics: NTF_FAST_PROF=1 prints per-CTA-averaged pipeline wait cycles
   static unsigned long long* prof = nullptr;
   const bool profiling = std::getenv("NTF_FAST_PROF") != nullptr;

@@ -344,6 +344,31 @@ __global__ void __launch_bounds__(max_threads_es(A, B, int(sizeof(T))), 1) mttkr
       else
         off[i] = (m / p.m_box) * p.m_box * p.kbox + (m % p.m_box);  // element offset at k = 0
     }
+    // periodic FP64 flush of the FP32 accumulators (KW == 1: each output
+    // entry of the CTA belongs to exactly one lane, so no race)
+    double* const slab = (p.ctas_per_mtile == 1 ? p.out : p.partial) + (size_t(j) * v.I) * r;
+    bool flushed = false;
+    int since_flush = 0;
+    auto flush_acc = [&]() {
+#pragma unroll
+      for (int i = 0; i < A; ++i) {
+        const int m = lane_row(i);
+        const long long row = (long long)mt * p.m_cta + m;
+        if (m < p.m_cta && row < v.I) {
+#pragma unroll
+          for (int b = 0; b < B; ++b) {
+            const int c = cg * B + b;
+            if (c < r) {
+              double* q = slab + row * r + c;
+              *q = flushed ? *q + double(acc[i][b]) : double(acc[i][b]);
+            }
+          }
+        }
+#pragma unroll
+        for (int b = 0; b < B; ++b) acc[i][b] = T(0);
+      }
+      flushed = true;
+    };
     int s = 0;
     uint32_t phase = 0;
     long long cw_full = 0;
@@ -419,6 +444,10 @@ __global__ void __launch_bounds__(max_threads_es(A, B, int(sizeof(T))), 1) mttkr
         s = 0;
         phase ^= 1;
       }
+      if (p.flush_units > 0 && ++since_flush == p.flush_units) {
+        since_flush = 0;
+        flush_acc();
+      }
     }
 
     if (prof_on && cw == 0 && lane == 0) {
@@ -465,7 +494,7 @@ __global__ void __launch_bounds__(max_threads_es(A, B, int(sizeof(T))), 1) mttkr
 #pragma unroll
           for (int b = 0; b < B; ++b) {
             const int c = cg * B + b;
-            if (c < r) out[row * r + c] = double(acc[i][b]);
+            if (c < r) out[row * r + c] = flushed ? out[row * r + c] + double(acc[i][b]) : double(acc[i][b]);
           }
         }
       }

@@ -47,6 +47,11 @@ struct Params {
   int bq[kMaxBase];      // their modes
   int qL, rowL_wrap;     // last varying mode; its row after a wrap
   unsigned long long* prof;  // optional per-CTA cycle counters (diagnostics), kProfSlots each
+  // FP32 tensors with long reductions: every flush_units units (KW == 1 only)
+  // each consumer lane adds its FP32 accumulators into its rows of the
+  // CTA's FP64 slab and restarts them, so no FP32 sum runs over more than
+  // flush_units * kbox terms (0: accumulate the whole range in registers)
+  int flush_units;
 };
 using LaunchFn = void (*)(const CUtensorMap& map, const Params& p, int grid, int threads, size_t smem,
                           cudaStream_t s);

@@ -149,3 +149,34 @@ def test_no_cpu_fallback_without_device(P):
         P.Context(0)
     with pytest.raises(P.CudaError):
         P.GpuDenseProvider(np.ones((2, 2, 2)))
+
+
+@pytest.mark.parametrize("shape,rank,sigma,dtype", [([9, 7, 5], 3, 0.05, np.float64), ([13, 4, 6, 3], 2, 0.1, np.float32),
+                                                    ([11, 6], 4, 0.0, np.float64), ([7], 2, 0.2, np.float64)])
+def test_generate_slab_matches_whole_instance(P, shape, rank, sigma, dtype):
+    """ntf_generate_slab: every mode-1 slab (the part a sharded rank holds)
+    is bit-identical to that slice of the whole instance, noise included
+    (the parallel generator enters the serial noise stream at the slab's
+    first entry)."""
+    spec = P.SyntheticSpec(shape=shape, rank=rank, noise_sigma=sigma, seed=77)
+    whole, truth = P.generate(spec, dtype=dtype)
+    for world in (1, 2, 3, 4):
+        for r in range(world):
+            b, e = P.slab_range(shape[0], r, world)
+            part, truth2 = P.generate(spec, dtype=dtype, slab=(b, e))
+            assert part.shape == tuple([e - b] + shape[1:])
+            assert np.array_equal(part, whole[b:e])
+            assert all(np.array_equal(x, y) for x, y in zip(truth2, truth))
+    with pytest.raises(P.InvalidArgument):
+        P.generate(spec, dtype=dtype, slab=(0, shape[0] + 1))
+
+
+def test_generate_large_chunked_noise_matches_oracle(P, oracle):
+    """More entries than one generator chunk (2^20), so several OpenMP
+    workers start from producer snapshots of the noise stream: still
+    bit-exact with the serial oracle."""
+    shape, rank = [40, 160, 200], 3
+    spec = P.SyntheticSpec(shape=shape, rank=rank, noise_sigma=0.3, seed=5)
+    t, _ = P.generate(spec)
+    ref, _ = oracle.generate(shape, rank, 0.3, False, 5)
+    assert np.array_equal(t, ref)
