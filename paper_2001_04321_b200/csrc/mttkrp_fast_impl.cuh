@@ -444,9 +444,11 @@ __global__ void __launch_bounds__(max_threads_es(A, B, int(sizeof(T))), 1) mttkr
         s = 0;
         phase ^= 1;
       }
-      if (p.flush_units > 0 && ++since_flush == p.flush_units) {
-        since_flush = 0;
-        flush_acc();
+      if constexpr (sizeof(T) == 4) {  // FP32 only (FP64 sums need no flush)
+        if (p.flush_units > 0 && ++since_flush == p.flush_units) {
+          since_flush = 0;
+          flush_acc();
+        }
       }
     }
 
@@ -494,7 +496,12 @@ __global__ void __launch_bounds__(max_threads_es(A, B, int(sizeof(T))), 1) mttkr
 #pragma unroll
           for (int b = 0; b < B; ++b) {
             const int c = cg * B + b;
-            if (c < r) out[row * r + c] = flushed ? out[row * r + c] + double(acc[i][b]) : double(acc[i][b]);
+            if (c < r) {
+              if (sizeof(T) == 4 && flushed)
+                out[row * r + c] += double(acc[i][b]);
+              else
+                out[row * r + c] = double(acc[i][b]);
+            }
           }
         }
       }
