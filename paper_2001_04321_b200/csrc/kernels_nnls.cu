@@ -728,7 +728,37 @@ __global__ void __launch_bounds__(kStreamTPB, 1) nnls_stream_kernel(NnlsLaunch a
   cg::cluster_group cl = cg::this_cluster();
 
   RunState* st = a.st;
-  if (st && st->done) return;  // budget exhausted: the whole iteration is a no-op (uniform)
+  const int r = a.rank, mode = a.mode;
+  DevFactors* F = a.F;
+  // one round of global loads: the role bits, the budget flag and the
+  // driver scalars (the buffer pointers come with the launch: a.bufs)
+  int selv[kMaxOrder] = {};
+  const double* gp0[kMaxOrder] = {};
+  const double* gp1[kMaxOrder] = {};
+  double* xp0 = nullptr;
+  double* xp1 = nullptr;
+  int sel = 0, done = 0;
+  double beta = 0.0, tol = a.tol;
+  int max_iters = a.max_iters;
+  if (F) {
+    done = st->done;
+    beta = (a.role == 0) ? st->beta : 0.0;
+    max_iters = st->inner_max_iters;
+    tol = st->tol;
+#pragma unroll
+    for (int j = 0; j < kMaxOrder; ++j)
+      if (j < a.order) {
+        selv[j] = F->sel[j];
+        gp0[j] = a.has_bufs ? a.bufs.gram[j][0] : F->gram[j][0];
+        gp1[j] = a.has_bufs ? a.bufs.gram[j][1] : F->gram[j][1];
+      }
+    xp0 = a.has_bufs ? a.bufs.x[mode][0] : F->x[mode][0];
+    xp1 = a.has_bufs ? a.bufs.x[mode][1] : F->x[mode][1];
+#pragma unroll
+    for (int j = 0; j < kMaxOrder; ++j)
+      if (j == mode) sel = selv[j];
+  }
+  if (done) return;  // budget exhausted: the whole iteration is a no-op (uniform)
   const long long t_begin = clock64();
 
   const int nrw = int(blockDim.x >> 5) - 1;  // row warps; warp nrw reduces
@@ -751,62 +781,13 @@ __global__ void __launch_bounds__(kStreamTPB, 1) nnls_stream_kernel(NnlsLaunch a
   uint64_t* cbar = rowbar + D;                                // kStreamDC
   unsigned long long* ctl = reinterpret_cast<unsigned long long*>(cbar + kStreamDC);  // (stop << 32) | decided
 
-  const int r = a.rank, mode = a.mode;
-  DevFactors* F = a.F;
-  // pointer chase F -> sel / buffers in one round trip (both buffers' pointers, then select)
-  int selv[kMaxOrder];
-  const double* gp0[kMaxOrder];
-  const double* gp1[kMaxOrder];
-  double* xp0 = nullptr;
-  double* xp1 = nullptr;
-  int sel = 0;
-  if (F) {
-#pragma unroll
-    for (int j = 0; j < kMaxOrder; ++j)
-      if (j < a.order) {
-        selv[j] = F->sel[j];
-        gp0[j] = F->gram[j][0];
-        gp1[j] = F->gram[j][1];
-      }
-    xp0 = F->x[mode][0];
-    xp1 = F->x[mode][1];
-#pragma unroll
-    for (int j = 0; j < kMaxOrder; ++j)
-      if (j == mode) sel = selv[j];
-  }
   double* X = sel ? xp1 : xp0;
-  const double beta = (a.role == 0) ? st->beta : 0.0;
-  const int max_iters = (a.role == 2) ? a.max_iters : st->inner_max_iters;
-  const double tol = (a.role == 2) ? a.tol : st->tol;
   const double* w0 = (a.role == 2) ? a.w0 : X;
   const double* C = a.C;
 
-  // ---- G: Hadamard of the other modes' Grams (kernels.cpp:193-200).
-  // (global loads of four entries per thread in flight together)
-  for (int e0 = threadIdx.x; e0 < RP * RP; e0 += 4 * blockDim.x) {
-    double g[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int e = e0 + u * int(blockDim.x);
-      const int p = e / RP, q = e % RP;
-      g[u] = 0.0;
-      if (e < RP * RP && p < r && q < r) {
-        if (a.role == 2) {
-          g[u] = a.gram_in[p * r + q];
-        } else {
-          g[u] = 1.0;
-#pragma unroll
-          for (int j = 0; j < kMaxOrder; ++j)
-            if (j < a.order && j != mode) g[u] *= (selv[j] ? gp1[j] : gp0[j])[p * r + q];
-        }
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-      if (e0 + u * int(blockDim.x) < RP * RP) Gs[e0 + u * int(blockDim.x)] = g[u];
-  }
-  for (int e0 = threadIdx.x; e0 < nloc * RP; e0 += 4 * blockDim.x) {
-    double cv[4];
+  // rows of C: the first batch of loads is issued before the G loads (both
+  // round trips overlap); its stores follow the G loop
+  auto load_c = [&](int e0, double(&cv)[4]) {
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const int e = e0 + u * int(blockDim.x);
@@ -814,11 +795,52 @@ __global__ void __launch_bounds__(kStreamTPB, 1) nnls_stream_kernel(NnlsLaunch a
       const int gr = int(blockIdx.x) * rpc + i;
       cv[u] = (e < nloc * RP && i < rpc && gr < a.rows && l < r) ? C[(long long)gr * r + l] : 0.0;
     }
+  };
+  auto store_c = [&](int e0, const double(&cv)[4]) {
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const int e = e0 + u * int(blockDim.x);
       if (e < nloc * RP) Cs[(e / RP) * LDC + e % RP] = cv[u];
     }
+  };
+  double cv0[4];
+  load_c(int(threadIdx.x), cv0);
+  const long long t_q0 = clock64();
+  // ---- G: Hadamard of the other modes' Grams (kernels.cpp:193-200).
+  // (global loads of four entries per thread in flight together)
+  for (int e0 = threadIdx.x; e0 < RP * RP; e0 += 4 * blockDim.x) {
+    // every factor value first (independent read-only loads, all in flight),
+    // then the products in ascending mode order
+    double v[4][kMaxOrder];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int e = e0 + u * int(blockDim.x);
+      const int p = e / RP, q = e % RP;
+      const bool in = e < RP * RP && p < r && q < r;
+#pragma unroll
+      for (int j = 0; j < kMaxOrder; ++j) {
+        const bool use = in && (a.role == 2 ? j == 0 : (j < a.order && j != mode));
+        const double* src = a.role == 2 ? a.gram_in : (selv[j] ? gp1[j] : gp0[j]);
+        v[u][j] = use ? __ldg(src + p * r + q) : 1.0;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int e = e0 + u * int(blockDim.x);
+      const int p = e / RP, q = e % RP;
+      double g = 1.0;
+#pragma unroll
+      for (int j = 0; j < kMaxOrder; ++j) g *= v[u][j];
+      if (e < RP * RP) Gs[e] = (p < r && q < r) ? g : 0.0;
+    }
+  }
+  const long long t_q1 = clock64();
+  store_c(int(threadIdx.x), cv0);
+  const long long t_q2 = clock64();
+  for (int e0 = int(threadIdx.x) + 4 * int(blockDim.x); e0 < nloc * RP; e0 += 4 * int(blockDim.x)) {
+    double cv[4];
+    load_c(e0, cv);
+    store_c(e0, cv);
   }
   if (threadIdx.x == 0) {
     for (int b = 0; b < D; ++b)
@@ -1066,9 +1088,10 @@ __global__ void __launch_bounds__(kStreamTPB, 1) nnls_stream_kernel(NnlsLaunch a
 
   // ---- write the block (HER: solved + extrapolated twin; AO: in place).
   const double* Wf = stash + fs * RP * nloc;  // [RP][nloc]
-  double* S = F->x[mode][sel ^ 1];
-  float* X32 = F->x32[mode][sel];
-  float* S32 = F->x32[mode][sel ^ 1];
+  double* S = sel ? xp0 : xp1;
+  const DevFactors& B = a.has_bufs ? a.bufs : *F;
+  float* X32 = B.x32[mode][sel];
+  float* S32 = B.x32[mode][sel ^ 1];
   for (int e0 = threadIdx.x; e0 < nloc * RP; e0 += 4 * blockDim.x) {
     double old[4];
 #pragma unroll
@@ -1103,33 +1126,45 @@ __global__ void __launch_bounds__(kStreamTPB, 1) nnls_stream_kernel(NnlsLaunch a
   }
   __syncthreads();
   const long long t_e1 = clock64();
-  // ---- Gram partials of this CTA's rows (W, and the twin for HER)
-  for (int e = threadIdx.x; e < RP * RP; e += blockDim.x) {
-    const int p = e / RP, q = e % RP;
-    if (p > q || q >= r) continue;
-    // four rows per step, two accumulator pairs per matrix (nloc % 4 == 0)
-    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0, h0 = 0.0, h1 = 0.0, h2 = 0.0, h3 = 0.0;
-    const double2* wp = reinterpret_cast<const double2*>(Wf + p * nloc);
-    const double2* wq = reinterpret_cast<const double2*>(Wf + q * nloc);
-    const double2* hp = reinterpret_cast<const double2*>(stage + p * nloc);
-    const double2* hq = reinterpret_cast<const double2*>(stage + q * nloc);
-    const bool twin = a.role == 0;
-    for (int i = 0; i < nloc / 2; i += 2) {
-      const double2 a0 = wp[i], a1 = wp[i + 1], b0 = wq[i], b1 = wq[i + 1];
-      s0 = fma(a0.x, b0.x, s0);
-      s1 = fma(a0.y, b0.y, s1);
-      s2 = fma(a1.x, b1.x, s2);
-      s3 = fma(a1.y, b1.y, s3);
-      if (twin) {
-        const double2 c0 = hp[i], c1 = hp[i + 1], d0 = hq[i], d1 = hq[i + 1];
-        h0 = fma(c0.x, d0.x, h0);
-        h1 = fma(c0.y, d0.y, h1);
-        h2 = fma(c1.x, d1.x, h2);
-        h3 = fma(c1.y, d1.y, h3);
+  // ---- Gram partials of this CTA's rows (W, and the twin for HER): one
+  // 2 x 2 block of entries per task, two accumulators per entry (even / odd
+  // rows), columns of the [RP][nloc] buffers read as double2
+  {
+    constexpr int NB = RP / 2;
+    constexpr int NBLK = NB * (NB + 1) / 2;  // blocks on or above the diagonal
+    const int nmat = (a.role == 0) ? 2 : 1;
+    for (int t = threadIdx.x; t < nmat * NBLK; t += blockDim.x) {
+      const int mat = t / NBLK;
+      int bi = t % NBLK, pb = 0;
+      while (bi >= NB - pb) {
+        bi -= NB - pb;
+        ++pb;
       }
+      const int p = 2 * pb, q = 2 * (pb + bi);
+      if (p >= r) continue;
+      const double* base = mat ? stage : Wf;
+      const double2* x0 = reinterpret_cast<const double2*>(base + p * nloc);
+      const double2* x1 = reinterpret_cast<const double2*>(base + (p + 1) * nloc);
+      const double2* y0 = reinterpret_cast<const double2*>(base + q * nloc);
+      const double2* y1 = reinterpret_cast<const double2*>(base + (q + 1) * nloc);
+      double e00 = 0.0, e01 = 0.0, e10 = 0.0, e11 = 0.0, o00 = 0.0, o01 = 0.0, o10 = 0.0, o11 = 0.0;
+      for (int i = 0; i < nloc / 2; ++i) {
+        const double2 a0 = x0[i], a1 = x1[i], b0 = y0[i], b1 = y1[i];
+        e00 = fma(a0.x, b0.x, e00);
+        o00 = fma(a0.y, b0.y, o00);
+        e01 = fma(a0.x, b1.x, e01);
+        o01 = fma(a0.y, b1.y, o01);
+        e10 = fma(a1.x, b0.x, e10);
+        o10 = fma(a1.y, b0.y, o10);
+        e11 = fma(a1.x, b1.x, e11);
+        o11 = fma(a1.y, b1.y, o11);
+      }
+      double* dst = part + mat * RP * RP;
+      dst[p * RP + q] = e00 + o00;
+      if (q + 1 < RP) dst[p * RP + q + 1] = e01 + o01;
+      if (p + 1 <= q) dst[(p + 1) * RP + q] = e10 + o10;
+      if (q + 1 < RP) dst[(p + 1) * RP + q + 1] = e11 + o11;
     }
-    part[e] = (s0 + s1) + (s2 + s3);
-    if (twin) part[RP * RP + e] = (h0 + h1) + (h2 + h3);
   }
   if (a.last) {
     // <W, C> and <W^T W, G> of this CTA (the cheap objective's data terms)
@@ -1153,8 +1188,8 @@ __global__ void __launch_bounds__(kStreamTPB, 1) nnls_stream_kernel(NnlsLaunch a
   const long long t_e2 = clock64();
   cl.sync();  // partials visible cluster-wide
   const long long t_e3 = clock64();
-  double* gW = (a.role == 0) ? F->gram[mode][sel ^ 1] : F->gram[mode][sel];
-  double* gH = F->gram[mode][sel];
+  double* gW = (a.role == 0) ? B.gram[mode][sel ^ 1] : B.gram[mode][sel];
+  double* gH = B.gram[mode][sel];
   const int nmat = (a.role == 0) ? 2 : 1;
   for (int e = int(threadIdx.x) * int(ncta) + int(me); e < nmat * RP * RP; e += int(blockDim.x) * int(ncta)) {
     const int mat = e / (RP * RP), pq = e % (RP * RP);
@@ -1200,6 +1235,9 @@ __global__ void __launch_bounds__(kStreamTPB, 1) nnls_stream_kernel(NnlsLaunch a
     ph[5] += t_e3 - t_e2;
     ph[6] += t_e4 - t_e3;
     ph[7] += t_end - t_e4;
+    ph[8] += t_q0 - t_begin;
+    ph[9] += t_q1 - t_q0;
+    ph[10] += t_q2 - t_q1;
     g_nnls_prof[0] += t_loop_end - t_loop;
     g_nnls_prof[1] += t_loop - t_begin;
     g_nnls_prof[2] += s;

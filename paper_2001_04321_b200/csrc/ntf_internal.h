@@ -134,6 +134,11 @@ struct NnlsLaunch {
   double tol;
   double* scratch;  // >= grid * (kMaxRank*kMaxRank + 64) doubles
   unsigned int* counter;
+  // drivers: the buffers behind F (fixed for a session), so the kernel only
+  // loads the role bits sel[] from device memory (hF: host copy of *F)
+  const DevFactors* hF;
+  DevFactors bufs;
+  int has_bufs;
 };
 void launch_nnls(const NnlsLaunch& a, cudaStream_t s);
 // diagnostics: {sweep-loop cycles, reduction cycles, sweeps, calls} of CTA 0

@@ -356,6 +356,8 @@ void Session::enqueue_iteration(bool timed) {
     a.st = st;
     a.trace = trace_.as<TraceEntry>();
     a.scratch = scratch_.as<double>();
+    a.bufs = hF_;
+    a.has_bufs = 1;
     launch_nnls(a, stream_);
   }
 }

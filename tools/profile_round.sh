@@ -11,6 +11,7 @@ $CMD > $O/plain_$R.log 2>&1 && \
   ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_$R.csv $CMD > $O/ncu_launch_$R.log 2>&1
 echo "launch list rc=$?"
 $CMD > $O/plain2_$R.log 2>&1 && \
-  ncu --set full --clock-control none --import-source on -k regex:"mttkrp_fast|nnls_kernel|tree_mttkrp" -s 12 -c 6 \
+  ncu --set full --clock-control none --import-source on -k regex:"mttkrp_fast|nnls_stream|tree_mttkrp" -s 12 -c 6 \
       -f -o $O/prof_$R $CMD > $O/ncu_full_$R.log 2>&1
 echo "full capture rc=$?"
+for c in c3 c4; do python bench.py --config $c --no-cpu-baseline > $O/bench_${c}_$R.json 2> $O/bench_${c}_$R.err; echo "bench $c rc=$?"; done
