@@ -724,6 +724,7 @@ __global__ void __launch_bounds__(kStreamTPB, 1) nnls_stream_kernel(NnlsLaunch a
   using SS = StreamShape<RP, Q, L>;
   constexpr int PQ = SS::PQ, PQ2 = SS::PQ2, WN2 = SS::WN2, D = SS::D;
   constexpr int LDC = RP + 1;
+  constexpr int LDW = RP + 2;  // row stride of the stash / twin buffers (16-byte rows)
   extern __shared__ __align__(16) double smem[];
   cg::cluster_group cl = cg::this_cluster();
 
@@ -770,10 +771,10 @@ __global__ void __launch_bounds__(kStreamTPB, 1) nnls_stream_kernel(NnlsLaunch a
   double2* wins = pushc + RP * PQ2 * Q;               // [RP][WN2]: h_{j,j+d}, d = 1..L-1 (window terms)
   double* Gs = reinterpret_cast<double*>(wins + RP * WN2);  // RP*RP
   double* Ginv = Gs + RP * RP;                             // RP
-  double* stash = Ginv + RP;                               // [D][RP][nloc]: W after each sweep
-  double* Cs = stash + D * RP * nloc;                      // [nloc][LDC]: rows of C
-  double* stage = Cs + nloc * LDC;                         // [RP][nloc]: extrapolated twin
-  double* part = stage + RP * nloc;                        // 2*RP*RP + 2: Gram partials, <W,C>, quad
+  double* stash = Ginv + RP;                               // [D][nloc][LDW]: W after each sweep
+  double* Cs = stash + D * nloc * LDW;                     // [nloc][LDC]: rows of C
+  double* stage = Cs + nloc * LDC;                         // [nloc][LDW]: extrapolated twin
+  double* part = stage + nloc * LDW;                       // 2*RP*RP + 2: Gram partials, <W,C>, quad
   double* d2part = part + 2 * RP * RP + 2;                 // [D][nloc]: per-row ||dW||^2
   double* cslot = d2part + D * nloc;                       // [kStreamDC][kMaxCluster]
   double* red = cslot + kStreamDC * kMaxCluster;           // 32
@@ -925,6 +926,13 @@ __global__ void __launch_bounds__(kStreamTPB, 1) nnls_stream_kernel(NnlsLaunch a
       for (int d = L - 1; d >= 2; --d)
         if (d > c) acc[c] = fma(-win((c - d + RP) % RP, d), Wl[(c - d + RP) % RP], acc[c]);
     }
+    if constexpr (L >= Q) {
+      // groups whose restart step (m Q + Q - 1 - L) precedes sweep 0 have
+      // just handed over their initial sums: they restart now
+#pragma unroll
+      for (int m = 0; m < PQ; ++m)
+        if (m * Q + Q - 1 - L < 0) P[m] = rv[m];
+    }
     // coefficient registers of the next two steps (rows j of pushc / wins)
     double2 pcr[RP][PQ2], wr[RP][WN2];
     auto load_row = [&](int j) {
@@ -962,14 +970,14 @@ __global__ void __launch_bounds__(kStreamTPB, 1) nnls_stream_kernel(NnlsLaunch a
         if (c >> 32) break;
       }
       double d2 = 0.0;
-      double* stp = stash + ((s + D - 1) % D) * RP * nloc + slot;  // slot of sweep s - 1
+      double* stp = stash + (((s + D - 1) % D) * nloc + slot) * LDW;  // row of sweep s - 1
       const long long tp0 = pclock();
 #pragma unroll
       for (int j = 0; j < RP; ++j) {
         const int jm1 = (j + RP - 1) % RP;
         const double v = fma(-wcoef(jm1, 1), Wl[jm1], acc[j]);
         const double nw = clip_mask(v, -int((okbits >> j) & 1u));
-        if (k == 0) stp[j * nloc] = Wl[j];
+        if (k == 0) stp[j] = Wl[j];
         const double dd = nw - Wl[j];
         d2 = fma(dd, dd, d2);
         Wl[j] = nw;
@@ -977,8 +985,18 @@ __global__ void __launch_bounds__(kStreamTPB, 1) nnls_stream_kernel(NnlsLaunch a
         for (int d = 2; d < L; ++d) acc[(j + d) % RP] = fma(-wcoef(j, d), nw, acc[(j + d) % RP]);
 #pragma unroll
         for (int m = 0; m < PQ; ++m) P[m] = fma(-nw, pcoef(j, m), P[m]);
-        if (k == j % Q) P[j / Q] = rv[j / Q];
         acc[(j + L) % RP] = bcast(P[((j + L) % RP) / Q], (j + L) % RP);
+        if constexpr (L >= Q) {
+          // every sum of the column group m is idle from its hand-over (L
+          // steps before it is due) until after its evaluation, so the
+          // whole group restarts at once, unconditionally, right after the
+          // last of the group's hand-overs (step m Q + Q - 1 - L)
+#pragma unroll
+          for (int m = 0; m < PQ; ++m)
+            if (((m * Q + Q - 1 - L) % RP + RP) % RP == j) P[m] = rv[m];
+        } else {
+          if (k == j % Q) P[j / Q] = rv[j / Q];
+        }
         load_row((j + 2) % RP);
         if (j == RP / 2) c = ld_volatile_u64(ctl);  // decisions so far, checked after the pass
       }
@@ -994,9 +1012,9 @@ __global__ void __launch_bounds__(kStreamTPB, 1) nnls_stream_kernel(NnlsLaunch a
       ++passes;
     }
     if (k == 0) {  // the last sweep's result (or W0 when no sweep ran)
-      double* stp = stash + ((s + D - 1) % D) * RP * nloc + slot;
+      double* stp = stash + (((s + D - 1) % D) * nloc + slot) * LDW;
 #pragma unroll
-      for (int l = 0; l < RP; ++l) stp[l * nloc] = Wl[l];
+      for (int l = 0; l < RP; ++l) stp[l] = Wl[l];
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       g_nnls_prof[5] += passes;
@@ -1079,7 +1097,7 @@ __global__ void __launch_bounds__(kStreamTPB, 1) nnls_stream_kernel(NnlsLaunch a
     for (int e = threadIdx.x; e < nloc * RP; e += blockDim.x) {
       const int i = e / RP, l = e % RP;
       const int row = int(blockIdx.x) * rpc + i;
-      if (i < rpc && row < a.rows && l < r) a.w_out[(long long)row * r + l] = stash[(fs * RP + l) * nloc + i];
+      if (i < rpc && row < a.rows && l < r) a.w_out[(long long)row * r + l] = stash[(fs * nloc + i) * LDW + l];
     }
     if (blockIdx.x == 0 && threadIdx.x == 0 && a.sweeps_out) *a.sweeps_out = s;
     cl.sync();  // no CTA leaves while cluster traffic may target it
@@ -1087,7 +1105,7 @@ __global__ void __launch_bounds__(kStreamTPB, 1) nnls_stream_kernel(NnlsLaunch a
   }
 
   // ---- write the block (HER: solved + extrapolated twin; AO: in place).
-  const double* Wf = stash + fs * RP * nloc;  // [RP][nloc]
+  const double* Wf = stash + fs * nloc * LDW;  // [nloc][LDW]
   double* S = sel ? xp0 : xp1;
   const DevFactors& B = a.has_bufs ? a.bufs : *F;
   float* X32 = B.x32[mode][sel];
@@ -1107,7 +1125,7 @@ __global__ void __launch_bounds__(kStreamTPB, 1) nnls_stream_kernel(NnlsLaunch a
       if (e >= nloc * RP) break;
       const int i = e / RP, l = e % RP;
       const int row = int(blockIdx.x) * rpc + i;
-      const double w = Wf[l * nloc + i];
+      const double w = Wf[i * LDW + l];
       double h = 0.0;
       if (i < rpc && row < a.rows && l < r) {
         const long long o = (long long)row * r + l;
@@ -1121,7 +1139,7 @@ __global__ void __launch_bounds__(kStreamTPB, 1) nnls_stream_kernel(NnlsLaunch a
         X[o] = h;
         if (X32) X32[o] = float(h);
       }
-      if (a.role == 0) stage[l * nloc + i] = h;
+      if (a.role == 0) stage[i * LDW + l] = h;
     }
   }
   __syncthreads();
@@ -1143,20 +1161,19 @@ __global__ void __launch_bounds__(kStreamTPB, 1) nnls_stream_kernel(NnlsLaunch a
       const int p = 2 * pb, q = 2 * (pb + bi);
       if (p >= r) continue;
       const double* base = mat ? stage : Wf;
-      const double2* x0 = reinterpret_cast<const double2*>(base + p * nloc);
-      const double2* x1 = reinterpret_cast<const double2*>(base + (p + 1) * nloc);
-      const double2* y0 = reinterpret_cast<const double2*>(base + q * nloc);
-      const double2* y1 = reinterpret_cast<const double2*>(base + (q + 1) * nloc);
       double e00 = 0.0, e01 = 0.0, e10 = 0.0, e11 = 0.0, o00 = 0.0, o01 = 0.0, o10 = 0.0, o11 = 0.0;
-      for (int i = 0; i < nloc / 2; ++i) {
-        const double2 a0 = x0[i], a1 = x1[i], b0 = y0[i], b1 = y1[i];
+      for (int i = 0; i < nloc; i += 2) {
+        const double2 a0 = *reinterpret_cast<const double2*>(base + i * LDW + p);
+        const double2 b0 = *reinterpret_cast<const double2*>(base + i * LDW + q);
+        const double2 a1 = *reinterpret_cast<const double2*>(base + (i + 1) * LDW + p);
+        const double2 b1 = *reinterpret_cast<const double2*>(base + (i + 1) * LDW + q);
         e00 = fma(a0.x, b0.x, e00);
-        o00 = fma(a0.y, b0.y, o00);
-        e01 = fma(a0.x, b1.x, e01);
-        o01 = fma(a0.y, b1.y, o01);
-        e10 = fma(a1.x, b0.x, e10);
-        o10 = fma(a1.y, b0.y, o10);
-        e11 = fma(a1.x, b1.x, e11);
+        e01 = fma(a0.x, b0.y, e01);
+        e10 = fma(a0.y, b0.x, e10);
+        e11 = fma(a0.y, b0.y, e11);
+        o00 = fma(a1.x, b1.x, o00);
+        o01 = fma(a1.x, b1.y, o01);
+        o10 = fma(a1.y, b1.x, o10);
         o11 = fma(a1.y, b1.y, o11);
       }
       double* dst = part + mat * RP * RP;
@@ -1172,7 +1189,7 @@ __global__ void __launch_bounds__(kStreamTPB, 1) nnls_stream_kernel(NnlsLaunch a
     double cr = 0.0, qd = 0.0;
     for (int e = threadIdx.x; e < nloc * RP; e += blockDim.x) {
       const int i = e / RP, l = e % RP;
-      if (l < r) cr += Wf[l * nloc + i] * Cs[i * LDC + l];
+      if (l < r) cr += Wf[i * LDW + l] * Cs[i * LDC + l];
     }
     for (int e = threadIdx.x; e < RP * RP; e += blockDim.x) {
       const int p = e / RP, q = e % RP;
@@ -1294,7 +1311,7 @@ bool launch_stream_q(const NnlsLaunch& a, cudaStream_t s) {
   if (threads > kStreamTPB) return false;
   const size_t nloc = size_t(roww) * 32 / Q;
   const size_t smem = sizeof(double2) * (RP * SS::PQ2 * Q + RP * SS::WN2) +
-                      sizeof(double) * (RP * RP + RP + SS::D * RP * nloc + nloc * (RP + 1) + RP * nloc +
+                      sizeof(double) * (RP * RP + RP + SS::D * nloc * (RP + 2) + nloc * (RP + 1) + nloc * (RP + 2) +
                                         2 * RP * RP + 2 + SS::D * nloc + kStreamDC * kMaxCluster + 32) +
                       sizeof(uint64_t) * (SS::D + kStreamDC + 1);
   auto fn = nnls_stream_kernel<RP, Q, L>;
