@@ -552,20 +552,22 @@ __global__ void __launch_bounds__(max_threads_es(A, B, int(sizeof(T))), 1) mttkr
       for (long long eb = e0; eb < e1; eb += n_oct) {
         const long long e = eb + oct;
         const bool ok = e < e1;
-        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-        int q = t8;
-#pragma unroll 4
-        for (; q + 24 < nsl; q += 32) {
-          const double x0 = ok ? __ldcg(p.partial + (size_t(q) * n + e)) : 0.0;
-          const double x1 = ok ? __ldcg(p.partial + (size_t(q + 8) * n + e)) : 0.0;
-          const double x2 = ok ? __ldcg(p.partial + (size_t(q + 16) * n + e)) : 0.0;
-          const double x3 = ok ? __ldcg(p.partial + (size_t(q + 24) * n + e)) : 0.0;
-          s0 += x0;
-          s1 += x1;
-          s2 += x2;
-          s3 += x3;
+        // up to 24 slabs per lane loaded in one round (148 slabs: 19)
+        double x[24];
+#pragma unroll
+        for (int u = 0; u < 24; ++u) {
+          const int q = t8 + 8 * u;
+          x[u] = (ok && q < nsl) ? __ldcg(p.partial + (size_t(q) * n + e)) : 0.0;
         }
-        for (; q < nsl; q += 8) s0 += ok ? __ldcg(p.partial + (size_t(q) * n + e)) : 0.0;
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+        for (int u = 0; u < 24; u += 4) {
+          s0 += x[u];
+          s1 += x[u + 1];
+          s2 += x[u + 2];
+          s3 += x[u + 3];
+        }
+        for (int q = t8 + 8 * 24; q < nsl; q += 8) s0 += ok ? __ldcg(p.partial + (size_t(q) * n + e)) : 0.0;
         double sum = (s0 + s1) + (s2 + s3);
         sum += __shfl_xor_sync(0xffffffffu, sum, 1);
         sum += __shfl_xor_sync(0xffffffffu, sum, 2);
