@@ -145,6 +145,16 @@ int ntf_generate(const int* shape, int order, int rank, double sigma, int ill_co
 int ntf_generate_slab(const int* shape, int order, int rank, double sigma, int ill_conditioned,
                       int collinear, uint64_t seed, int dtype, int64_t slab_begin, int64_t slab_end,
                       void* tensor_out, double* truth_out);
+/* NTFT container on the host (tensor.cpp:56-96; README "File formats").
+ * info: order and dims (shape has room for 8). read: rows [slab_begin,
+ * slab_end) of mode 1 (-1, -1: all) as dtype (FP32 = round to nearest of the
+ * FP64 payload). write = DenseTensor::save (FP32 data is written exactly
+ * upcast). Errors as DenseTensor::load: NTF_ERR_RUNTIME with the same text
+ * ("cannot open", "not a tensor container", "unsupported version",
+ * "bad order", "truncated payload"). */
+int ntf_ntft_info(const char* path, int* order, int64_t* shape);
+int ntf_ntft_read(const char* path, int dtype, int64_t slab_begin, int64_t slab_end, void* out);
+int ntf_ntft_write(const char* path, const void* data, int dtype, int order, const int64_t* shape);
 /* factor_error (src/metrics.cpp:79-111). */
 int ntf_factor_error(const double* est, const double* truth, const int* shape, int order, int rank,
                      double* out);
@@ -177,6 +187,11 @@ int ntf_tensor_upload_device(ntf_ctx* ctx, const void* dev, int dtype, int order
 int ntf_tensor_shape(const ntf_tensor* t, int* order, int64_t* shape);
 int ntf_tensor_norm_sq(const ntf_tensor* t, double* out);
 int ntf_tensor_destroy(ntf_tensor* t);
+/* DenseTensor::load from the reference's binary container (tensor.cpp:73-96,
+ * magic "NTFT", u32 version 1, u32 order, u64 dims, FP64 payload): this
+ * rank's mode-1 slab is read (one seek) and streamed to the device through
+ * pinned staging buffers, rounded to FP32 when dtype is NTF_DTYPE_F32. */
+int ntf_tensor_upload_ntft(ntf_ctx* ctx, const char* path, int dtype, ntf_tensor** out);
 /* ObjectiveProvider::mttkrp (provider.hpp:18; kernels.cpp:161-191): out is
  * the I_mode x rank MTTKRP (row-major, FP64), identical on every rank. */
 int ntf_mttkrp(ntf_ctx* ctx, const ntf_tensor* t, const double* factors, int rank, int mode,

@@ -75,6 +75,10 @@ SIGNATURES = {
     "ntf_generate_slab": (C.c_int, [iptr, C.c_int, C.c_int, C.c_double, C.c_int, C.c_int, C.c_uint64, C.c_int,
                                     C.c_int64, C.c_int64, C.c_void_p, dptr]),
     "ntf_factor_error": (C.c_int, [dptr, dptr, iptr, C.c_int, C.c_int, dptr]),
+    "ntf_ntft_info": (C.c_int, [C.c_char_p, iptr, C.POINTER(C.c_int64)]),
+    "ntf_ntft_read": (C.c_int, [C.c_char_p, C.c_int, C.c_int64, C.c_int64, C.c_void_p]),
+    "ntf_ntft_write": (C.c_int, [C.c_char_p, C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_int64)]),
+    "ntf_tensor_upload_ntft": (C.c_int, [C.c_void_p, C.c_char_p, C.c_int, C.POINTER(C.c_void_p)]),
     "ntf_device_count": (C.c_int, [iptr]),
     "ntf_ctx_create": (C.c_int, [C.c_int, C.POINTER(C.c_void_p)]),
     "ntf_nccl_unique_id": (C.c_int, [C.c_char_p]),

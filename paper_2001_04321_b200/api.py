@@ -18,6 +18,7 @@ from __future__ import annotations
 import ctypes as C
 import dataclasses
 import enum
+import os
 import math
 from typing import Callable, List, Optional, Sequence
 
@@ -321,6 +322,38 @@ def generate(spec: SyntheticSpec, dtype=np.float64, slab=None):
     return t.reshape([e - b] + shape[1:]), KruskalModel.from_flat(truth, shape, spec.rank)
 
 
+def ntft_info(path):
+    """Shape stored in an NTFT container (tensor.cpp:73-88)."""
+    order = C.c_int()
+    shape = (C.c_int64 * 8)()
+    _check(L.lib().ntf_ntft_info(os.fsencode(path), C.byref(order), shape))
+    return [int(shape[i]) for i in range(order.value)]
+
+
+def save_tensor(path, tensor):
+    """DenseTensor::save (tensor.cpp:56-71): NTFT container, FP64 payload
+    (FP32 data is written exactly upcast)."""
+    t = np.ascontiguousarray(tensor)
+    if t.dtype not in (np.float32, np.float64):
+        t = t.astype(np.float64)
+    code = L.NTF_DTYPE_F32 if t.dtype == np.float32 else L.NTF_DTYPE_F64
+    shape = (C.c_int64 * t.ndim)(*t.shape)
+    _check(L.lib().ntf_ntft_write(os.fsencode(path), t.ctypes.data_as(C.c_void_p), code, t.ndim, shape))
+
+
+def load_tensor(path, dtype=np.float64, slab=None):
+    """DenseTensor::load (tensor.cpp:73-96); ``slab=(b, e)`` reads only the
+    mode-1 rows [b, e) (one seek), ``dtype=np.float32`` rounds to nearest."""
+    shape = ntft_info(path)
+    b, e = (0, shape[0]) if slab is None else (int(slab[0]), int(slab[1]))
+    if not 0 <= b <= e <= shape[0]:
+        raise InvalidArgument("slab outside the first mode")
+    out = np.empty([e - b] + shape[1:], dtype=np.float32 if np.dtype(dtype) == np.float32 else np.float64)
+    code = L.NTF_DTYPE_F32 if out.dtype == np.float32 else L.NTF_DTYPE_F64
+    _check(L.lib().ntf_ntft_read(os.fsencode(path), code, b, e, out.ctypes.data_as(C.c_void_p)))
+    return out
+
+
 def factor_error(est, truth) -> float:
     """src/metrics.cpp:79-111."""
     est, truth = _as_model(est), _as_model(truth)
@@ -436,6 +469,21 @@ class GpuDenseProvider(ObjectiveProvider):
         self.handle = h
         self._shape = [int(d) for d in shape]
         self.dtype = np.float32 if code == L.NTF_DTYPE_F32 else np.float64
+
+    @classmethod
+    def from_ntft(cls, path, ctx: Optional[Context] = None, dtype=np.float64):
+        """DenseTensor::load (tensor.cpp:73-96) straight to the device: this
+        rank's mode-1 slab is read from the NTFT container and streamed
+        through pinned staging buffers (FP32: round to nearest)."""
+        self = cls.__new__(cls)
+        self.ctx = ctx or default_context()
+        code = L.NTF_DTYPE_F32 if np.dtype(dtype) == np.float32 else L.NTF_DTYPE_F64
+        h = C.c_void_p()
+        _check(L.lib().ntf_tensor_upload_ntft(self.ctx.handle, os.fsencode(path), code, C.byref(h)))
+        self.handle = h
+        self._shape = ntft_info(path)
+        self.dtype = np.float32 if code == L.NTF_DTYPE_F32 else np.float64
+        return self
 
     def shape(self):
         return list(self._shape)

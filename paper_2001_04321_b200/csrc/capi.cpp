@@ -93,10 +93,12 @@ void check_run_inputs(const ntf_tensor* t, const double* init, int rank, const n
   if (cfg.inner_stop.max_iters < 0) throw InvalidArgument("inner max_iters must be >= 0");
 }
 
-ntf_tensor* make_tensor(ntf_ctx* ctx, const void* src, bool src_on_device, int dtype, int order,
-                        const int64_t* shape) {
+// The tensor handle of this rank's mode-1 slab; `fill` copies the slab's
+// n_local values into t->data on ctx->stream. ||T||^2 follows (FP64,
+// all-reduced over the ranks).
+template <typename Fill>
+ntf_tensor* make_tensor_with(ntf_ctx* ctx, int dtype, int order, const int64_t* shape, Fill&& fill) {
   need(ctx, "ctx");
-  need(src, "tensor data");
   need(shape, "shape");
   if (dtype != NTF_DTYPE_F64 && dtype != NTF_DTYPE_F32) throw InvalidArgument("unknown dtype");
   if (order < 1 || order > NTF_MAX_ORDER) throw InvalidArgument("tensor order must lie in 1..8");
@@ -119,8 +121,7 @@ ntf_tensor* make_tensor(ntf_ctx* ctx, const void* src, bool src_on_device, int d
     const size_t es = dtype == NTF_DTYPE_F32 ? 4 : 8;
     NTF_CUDA(cudaSetDevice(ctx->device));
     t->data = DevBuf(size_t(t->n_local) * es);
-    NTF_CUDA(cudaMemcpyAsync(t->data.p, src, size_t(t->n_local) * es,
-                             src_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, ctx->stream));
+    fill(t);
     t->nsq_dev = DevBuf(sizeof(double));
     launch_norm_sq(t->data.p, dtype, t->n_local, ctx->scratch.as<double>(), int(ctx->scratch.bytes / 8),
                    t->nsq_dev.as<double>(), ctx->stream);
@@ -132,6 +133,16 @@ ntf_tensor* make_tensor(ntf_ctx* ctx, const void* src, bool src_on_device, int d
     throw;
   }
   return t;
+}
+
+ntf_tensor* make_tensor(ntf_ctx* ctx, const void* src, bool src_on_device, int dtype, int order,
+                        const int64_t* shape) {
+  need(src, "tensor data");
+  return make_tensor_with(ctx, dtype, order, shape, [&](ntf_tensor* t) {
+    const size_t es = dtype == NTF_DTYPE_F32 ? 4 : 8;
+    NTF_CUDA(cudaMemcpyAsync(t->data.p, src, size_t(t->n_local) * es,
+                             src_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, ctx->stream));
+  });
 }
 
 // A DevFactors over caller factors (sel = 0 for every mode), for the
@@ -418,6 +429,46 @@ int ntf_tensor_upload(ntf_ctx* ctx, const void* host, int dtype, int order, cons
   return guarded([&] {
     need(out, "out");
     *out = make_tensor(ctx, host, false, dtype, order, shape);
+  });
+}
+
+int ntf_tensor_upload_ntft(ntf_ctx* ctx, const char* path, int dtype, ntf_tensor** out) {
+  return guarded([&] {
+    need(out, "out");
+    need(path, "path");
+    const NtftHeader h = ntft_read_header(path);
+    *out = make_tensor_with(ctx, dtype, h.order, h.shape, [&](ntf_tensor* t) {
+      long long stride0 = 1;
+      for (int i = 1; i < h.order; ++i) stride0 *= h.shape[i];
+      ntft_stream_to_device(path, h, t->row0 * stride0, t->n_local, dtype, t->data.p, ctx->stream);
+    });
+  });
+}
+
+int ntf_ntft_info(const char* path, int* order, int64_t* shape) {
+  return guarded([&] {
+    need(path, "path");
+    const NtftHeader h = ntft_read_header(path);
+    if (order) *order = h.order;
+    if (shape)
+      for (int i = 0; i < h.order; ++i) shape[i] = h.shape[i];
+  });
+}
+
+int ntf_ntft_read(const char* path, int dtype, int64_t slab_begin, int64_t slab_end, void* out) {
+  return guarded([&] {
+    need(path, "path");
+    need(out, "out");
+    ntft_read_slab(path, dtype, slab_begin, slab_end, out);
+  });
+}
+
+int ntf_ntft_write(const char* path, const void* data, int dtype, int order, const int64_t* shape) {
+  return guarded([&] {
+    need(path, "path");
+    need(data, "data");
+    need(shape, "shape");
+    ntft_write(path, data, dtype, order, shape);
   });
 }
 

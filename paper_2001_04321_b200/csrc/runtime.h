@@ -23,6 +23,18 @@ void generate(const int* shape, int order, int rank, double sigma, int ill, int 
               int dtype, void* tensor, double* truth, long long slab_b = -1, long long slab_e = -1);
 double factor_error(const double* est, const double* truth, const int* shape, int order, int rank);
 
+// ---- NTFT container (tensor.cpp:56-96; ntft_io.cpp) -----------------------------
+struct NtftHeader {
+  int order = 0;
+  int64_t shape[kMaxOrder] = {};
+  int64_t payload_offset = 0;  // bytes
+};
+NtftHeader ntft_read_header(const std::string& path);
+void ntft_write(const std::string& path, const void* data, int dtype, int order, const int64_t* shape);
+void ntft_read_slab(const std::string& path, int dtype, int64_t slab_begin, int64_t slab_end, void* out);
+void ntft_stream_to_device(const std::string& path, const NtftHeader& h, long long first, long long count,
+                           int dtype, void* dst, cudaStream_t s);
+
 // ---- device memory ------------------------------------------------------------
 struct DevBuf {
   void* p = nullptr;
