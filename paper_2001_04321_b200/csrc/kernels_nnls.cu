@@ -960,14 +960,22 @@ __global__ void __launch_bounds__(kStreamTPB, 1) nnls_stream_kernel(NnlsLaunch a
     int s = 0;
     long long passes = 0, pass_cyc = 0;
     unsigned long long c = ld_volatile_u64(ctl);
-    for (;;) {
-      if (c >> 32) break;
+    long long gate_cyc = 0, gate_n = 0;
+    const long long rows_t0 = pclock();
+    // one sweep of the row (false: a stop was decided before it started);
+    // two per loop trip, so the rotating registers of Wl come back to their
+    // loop-entry allocation without a block of moves
+    auto one_pass = [&]() -> bool {
+      if (c >> 32) return false;
       if (s >= max_iters || (s >= D && int(c & 0xffffffffu) < s - D + 1)) {
+        const long long tg = pclock();
+        ++gate_n;
         do {
           __nanosleep(20);
           c = ld_volatile_u64(ctl);
         } while (!(c >> 32) && (s >= max_iters || int(c & 0xffffffffu) < s - D + 1));
-        if (c >> 32) break;
+        gate_cyc += pclock() - tg;
+        if (c >> 32) return false;
       }
       double d2 = 0.0;
       double* stp = stash + (((s + D - 1) % D) * nloc + slot) * LDW;  // row of sweep s - 1
@@ -1010,6 +1018,11 @@ __global__ void __launch_bounds__(kStreamTPB, 1) nnls_stream_kernel(NnlsLaunch a
       }
       ++s;
       ++passes;
+      return true;
+    };
+    for (;;) {
+      if (!one_pass()) break;
+      if (!one_pass()) break;
     }
     if (k == 0) {  // the last sweep's result (or W0 when no sweep ran)
       double* stp = stash + (((s + D - 1) % D) * nloc + slot) * LDW;
@@ -1019,6 +1032,9 @@ __global__ void __launch_bounds__(kStreamTPB, 1) nnls_stream_kernel(NnlsLaunch a
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       g_nnls_prof[5] += passes;
       g_nnls_prof[6] += pass_cyc;
+      g_nnls_prof[7] += gate_cyc;
+      g_nnls_skew[2][80] += gate_n;
+      g_nnls_skew[2][81] += pclock() - rows_t0;
     }
   } else {
     // -------------------------------------------------------- reducer warp

@@ -52,6 +52,7 @@ if _L.lib().ntf_debug_nnls_prof(_buf, 1) == 0 and _buf[3]:
               f"pass {tri / max(npass, 1):.0f} cyc), epilogue {pc / calls:.0f} cyc")
         ph = b[8 + 256 + 64: 8 + 256 + 72]
         ph2 = b[8 + 256 + 72: 8 + 256 + 75]
+        print("  row loop/call: total %.0f cyc, gate waits %.0f cyc in %.1f waits" % (b[8 + 256 + 81] / calls, _buf[7] / calls, b[8 + 256 + 80] / calls))
         print("  G+C detail/call: to C issue %.0f | G loop %.0f | C stores (wait) %.0f" % tuple(x / calls for x in ph2))
         print("  phases/call: G+C loads %.0f | tables %.0f | cl.sync %.0f || writes %.0f | gram part %.0f | cl.sync %.0f | reduce %.0f | cl.sync+ %.0f"
               % tuple(x / calls for x in ph))
