@@ -222,10 +222,11 @@ UnitModes unit_modes(const ModeView& v, int layout) {
 
 void fill_params_modes(const ModeView& v, int layout, fast::Params& p) {
   const UnitModes m = unit_modes(v, layout);
-  p.qL = m.qL;
-  if (v.last_factor >= 0 && m.qL == v.order - 1) p.qL = v.last_factor;  // dimension-tree view
+  // factor index of view dim q (merged-row views: dims q >= 1 are shifted)
+  const auto fac = [&](int q) { return q >= 1 ? q + v.fshift : q; };
+  p.qL = fac(m.qL);
   p.nb = m.nb;
-  for (int t = 0; t < fast::kMaxBase; ++t) p.bq[t] = m.bq[t];
+  for (int t = 0; t < fast::kMaxBase; ++t) p.bq[t] = t < m.nb ? fac(m.bq[t]) : m.bq[t];
   p.rowL_wrap = m.qL == 0 ? int(v.row0) : 0;
 }
 

@@ -79,21 +79,25 @@ struct ModeView {
   int dims[kMaxOrder];
   long long L, I, R;
   long long row0;
-  int last_factor = -1;  // factor index of the view's last mode when it is not that mode (dimension tree)
+  // dimension-tree views whose dim 0 is a merged row index: view dims q >= 1
+  // contract with factor q + fshift (Y_L = T x_h A_h ... x_{N-1} A_{N-1})
+  int fshift = 0;
 };
 
 // Dimension tree: Y = T x_{N-1} A_{N-1} (modes 0..N-2 of T, r trailing)
 // viewed around block `mode` as (L, I, R, r); see kernels_tree.cu.
 struct TreeView {
-  int order, mode, rank;  // order = N - 1
+  int order, mode, rank;  // order = number of tensor modes in the partial
   int dims[kMaxOrder];
   long long L, I, R;
   long long row0;
+  int foff = 0;  // view dim j contracts with factor j + foff (Y_R of a split tree)
 };
 int tree_chunks(const TreeView& v, int sms);
+int tree_tiles(const TreeView& v);
 // out (I x r) = block `mode`'s MTTKRP from Y; partial holds chunks * I * r doubles.
 void launch_tree_mttkrp(const double* Y, const TreeView& v, const DevFactors* dF, double* partial, int chunks,
-                        double* out, cudaStream_t s);
+                        unsigned* arrivals, double* out, cudaStream_t s);
 
 // ---- kernel launchers (CUDA translation units) ------------------------------
 struct MttkrpPlan;

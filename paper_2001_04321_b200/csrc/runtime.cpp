@@ -97,7 +97,7 @@ ModeView MttkrpEngine::view(int mode) const {
 }
 
 MttkrpEngine::MttkrpEngine(const ntf_ctx* ctx, const ntf_tensor* t, int rank, unsigned flags)
-    : ctx_(ctx), t_(t), rank_(rank), flags_(flags) {
+    : ctx_(ctx), t_(t), rank_(rank), flags_(flags), order_(t->order) {
   size_t need = 0;
   for (int m = 0; m < t->order; ++m) {
     const ModeView v = view(m);
@@ -111,34 +111,91 @@ MttkrpEngine::MttkrpEngine(const ntf_ctx* ctx, const ntf_tensor* t, int rank, un
   }
   if ((flags & NTF_RUN_DIMTREE) && !(flags & NTF_RUN_GENERIC) && t->order >= 3 &&
       view(t->order - 1).L < (1LL << 31)) {
-    ModeView tv{};
-    tv.order = 2;
-    tv.mode = 0;
-    tv.rank = rank;
-    const ModeView vlast = view(t->order - 1);
-    tv.dims[0] = int(vlast.L);  // rows of the output
-    tv.dims[1] = vlast.dims[t->order - 1];
-    tv.L = 1;
-    tv.I = vlast.L;
-    tv.R = vlast.I;
-    tv.row0 = 0;
-    tv.last_factor = t->order - 1;
-    const std::vector<int> tab = fast_mttkrp_unit_table(tv, t->dtype, ctx->sms);
+    // Split point h of the dimension tree: blocks 0..h-1 contract
+    // Y_L = T x_h A_h ... x_{N-1} A_{N-1} (previous sweep), blocks h..N-1
+    // contract Y_R = T x_0 A_0 ... x_{h-1} A_{h-1} (this sweep). h = N-1 is
+    // the one-sided tree (Y_R is block N-1's MTTKRP itself); 4-way tensors
+    // split in the middle so both partials are small (C3: 1.28 MB each
+    // instead of one 128 MB Y).
+    const int N = t->order;
+    int h = N >= 4 ? N / 2 : N - 1;
+    if (const char* e = std::getenv("NTF_TREE_SPLIT")) h = std::max(1, std::min(N - 1, std::atoi(e)));
+    const ModeView full = view(0);
+    const auto left_view = [&](int hh) {
+      ModeView tv{};
+      tv.order = 1 + (N - hh);
+      tv.mode = 0;
+      tv.rank = rank;
+      long long rows = 1;
+      for (int j = 0; j < hh; ++j) rows *= full.dims[j];
+      tv.dims[0] = int(rows);
+      for (int j = hh; j < N; ++j) tv.dims[1 + j - hh] = full.dims[j];
+      tv.L = 1;
+      tv.I = rows;
+      tv.R = 1;
+      for (int j = hh; j < N; ++j) tv.R *= full.dims[j];
+      tv.row0 = 0;
+      tv.fshift = hh - 1;
+      return tv;
+    };
+    const auto right_view = [&](int hh) {
+      ModeView rv{};
+      rv.order = hh + 1;
+      rv.mode = hh;
+      rv.rank = rank;
+      for (int j = 0; j < hh; ++j) rv.dims[j] = full.dims[j];
+      long long cols = 1;
+      for (int j = hh; j < N; ++j) cols *= full.dims[j];
+      rv.dims[hh] = int(cols);
+      rv.L = 1;
+      for (int j = 0; j < hh; ++j) rv.L *= full.dims[j];
+      rv.I = cols;
+      rv.R = 1;
+      rv.row0 = t->row0;
+      return rv;
+    };
+    std::vector<int> tab, rtab;
+    if (h < N - 1) {
+      long long cols = 1;
+      for (int j = h; j < N; ++j) cols *= full.dims[j];
+      if (cols < (1LL << 31)) {
+        tab = fast_mttkrp_unit_table(left_view(h), t->dtype, ctx->sms);
+        rtab = fast_mttkrp_unit_table(right_view(h), t->dtype, ctx->sms);
+      }
+      if (tab.empty() || rtab.empty()) h = N - 1;  // no fast plan for a split view: one-sided tree
+    }
+    if (h == N - 1) tab = fast_mttkrp_unit_table(left_view(h), t->dtype, ctx->sms);
     if (!tab.empty()) {
       tree_ = true;
-      ttm_view_ = tv;
+      split_ = h;
+      ttm_view_ = left_view(h);
       ttm_tab_ = DevBuf(tab.size() * sizeof(int));
       NTF_CUDA(cudaMemcpy(ttm_tab_.p, tab.data(), tab.size() * sizeof(int), cudaMemcpyHostToDevice));
-      ybuf_ = DevBuf(size_t(tv.I) * rank * sizeof(double));
-      need = std::max(need, fast_mttkrp_partial_len(tv, t->dtype, ctx->sms));
-      for (int m = 0; m + 1 < t->order; ++m) {
+      ybuf_ = DevBuf(size_t(ttm_view_.I) * rank * sizeof(double));
+      need = std::max(need, fast_mttkrp_partial_len(ttm_view_, t->dtype, ctx->sms));
+      if (h < N - 1) {
+        ttmr_view_ = right_view(h);
+        ttmr_tab_ = DevBuf(rtab.size() * sizeof(int));
+        NTF_CUDA(cudaMemcpy(ttmr_tab_.p, rtab.data(), rtab.size() * sizeof(int), cudaMemcpyHostToDevice));
+        yrbuf_ = DevBuf(size_t(ttmr_view_.I) * rank * sizeof(double));
+        need = std::max(need, fast_mttkrp_partial_len(ttmr_view_, t->dtype, ctx->sms));
+      }
+      int tiles = 1;
+      for (int m = 0; m < N; ++m) {
+        if (!tree_mode(m)) continue;
         const TreeView yv = tree_view(m);
         tree_chunks_[m] = tree_chunks(yv, ctx->sms);
+        tiles = std::max(tiles, tree_tiles(yv));
         need = std::max(need, size_t(tree_chunks_[m]) * size_t(yv.I) * rank);
       }
+      tree_tiles_max_ = tiles;
     }
   }
   partial_ = DevBuf(need * sizeof(double));
+  if (tree_) {
+    tree_arrivals_ = DevBuf(size_t(tree_tiles_max_) * sizeof(unsigned));
+    NTF_CUDA(cudaMemset(tree_arrivals_.p, 0, size_t(tree_tiles_max_) * sizeof(unsigned)));
+  }
   counter_ = DevBuf(2 * sizeof(unsigned));
   NTF_CUDA(cudaMemset(counter_.p, 0, 2 * sizeof(unsigned)));
   if (!(flags & NTF_RUN_GENERIC))
@@ -165,25 +222,31 @@ MttkrpEngine::MttkrpEngine(const ntf_ctx* ctx, const ntf_tensor* t, int rank, un
 }
 
 TreeView MttkrpEngine::tree_view(int mode) const {
+  // blocks < split_: Y_L over modes 0..split_-1; blocks >= split_: Y_R over
+  // modes split_..N-1 (factor offset split_, no slab offset)
   const ModeView v = view(mode);
+  const bool left = mode < split_;
+  const int lo = left ? 0 : split_, hi = left ? split_ : t_->order;
   TreeView y{};
-  y.order = t_->order - 1;
-  y.mode = mode;
+  y.order = hi - lo;
+  y.mode = mode - lo;
   y.rank = rank_;
-  for (int j = 0; j < y.order; ++j) y.dims[j] = v.dims[j];
+  for (int j = 0; j < y.order; ++j) y.dims[j] = v.dims[lo + j];
   y.L = 1;
   y.R = 1;
-  for (int j = 0; j < mode; ++j) y.L *= y.dims[j];
-  y.I = y.dims[mode];
-  for (int j = mode + 1; j < y.order; ++j) y.R *= y.dims[j];
-  y.row0 = t_->row0;
+  for (int j = 0; j < y.mode; ++j) y.L *= y.dims[j];
+  y.I = y.dims[y.mode];
+  for (int j = y.mode + 1; j < y.order; ++j) y.R *= y.dims[j];
+  y.row0 = left ? t_->row0 : 0;
+  y.foff = lo;
   return y;
 }
 
 std::string MttkrpEngine::describe(int mode) const {
-  if (tree_ && mode + 1 < t_->order)
-    return std::string("tree chunks=") + std::to_string(tree_chunks_[mode]) +
-           (mode == 0 ? " after TTM " + fast_mttkrp_describe(ttm_view_, t_->dtype, ctx_->sms) : std::string());
+  if (tree_mode(mode))
+    return std::string("tree split=") + std::to_string(split_) + " chunks=" + std::to_string(tree_chunks_[mode]) +
+           (mode == 0 ? " after Y_L " + fast_mttkrp_describe(ttm_view_, t_->dtype, ctx_->sms) : std::string()) +
+           (mode == split_ ? " after Y_R " + fast_mttkrp_describe(ttmr_view_, t_->dtype, ctx_->sms) : std::string());
   const ModeView v = view(mode);
   if (!(flags_ & NTF_RUN_GENERIC) && fast_mttkrp_supported(v, t_->dtype)) return fast_mttkrp_describe(v, t_->dtype, ctx_->sms);
   return "generic segs=" + std::to_string(segs_[mode]);
@@ -193,8 +256,9 @@ int MttkrpEngine::kernels_per_call(int mode) const {
   // the fast kernel reduces its split-K slabs itself (the engine passes an
   // arrival counter) unless NTF_FAST_SEPARATE_REDUCE asks for the old kernel
   const int fast_kernels = std::getenv("NTF_FAST_SEPARATE_REDUCE") ? 2 : 1;
-  if (tree_ && mode + 1 < t_->order)
-    return 2 + (mode == 0 ? std::min(fast_kernels, fast_mttkrp_kernels(ttm_view_, t_->dtype)) : 0);
+  if (tree_mode(mode))
+    return 1 + (mode == 0 ? std::min(fast_kernels, fast_mttkrp_kernels(ttm_view_, t_->dtype)) : 0) +
+           (mode == split_ ? std::min(fast_kernels, fast_mttkrp_kernels(ttmr_view_, t_->dtype)) : 0);
   const ModeView v = view(mode);
   if (!(flags_ & NTF_RUN_GENERIC) && fast_mttkrp_supported(v, t_->dtype))
     return std::min(fast_kernels, fast_mttkrp_kernels(v, t_->dtype));
@@ -207,13 +271,23 @@ void MttkrpEngine::run(int mode, const DevFactors* dF, double* out, cudaStream_t
   const Comm& comm = ctx_->comm;
   const bool gather = comm.world > 1 && mode == 0;
   double* dst = gather ? gather_.as<double>() + size_t(comm.rank) * maxrows_ * rank_ : out;
+  const bool seq = last_mode_ == mode - 1;
+  last_mode_ = mode;
   if (ev0) NTF_CUDA(cudaEventRecord(ev0, s));
-  if (tree_ && mode + 1 < t_->order) {
-    // block 0 opens the outer iteration: Y with this iteration's A_{N-1}
-    if (mode == 0)
+  if (tree_mode(mode)) {
+    // block 0 opens the outer iteration: Y_L with the previous sweep's
+    // A_split.. A_{N-1}; block split_ forms Y_R with this sweep's A_0..
+    // A partial is formed by the first block of its side; a block reached
+    // out of sweep order (the pivot objective's lone block N-1,
+    // driver_common.hpp:50-56) forms it with the current factors.
+    if (mode == 0 || (mode < split_ && !seq))
       fast_mttkrp(t_->data.p, t_->dtype, ttm_view_, dF, ttm_tab_.as<int>(), partial_.as<double>(), ybuf_.as<double>(),
                   ctx_->sms, s, counter_.as<unsigned>());
-    launch_tree_mttkrp(ybuf_.as<double>(), tree_view(mode), dF, partial_.as<double>(), tree_chunks_[mode], dst, s);
+    if (mode == split_ || (mode > split_ && !seq))
+      fast_mttkrp(t_->data.p, t_->dtype, ttmr_view_, dF, ttmr_tab_.as<int>(), partial_.as<double>(),
+                  yrbuf_.as<double>(), ctx_->sms, s, counter_.as<unsigned>());
+    launch_tree_mttkrp(mode < split_ ? ybuf_.as<double>() : yrbuf_.as<double>(), tree_view(mode), dF,
+                       partial_.as<double>(), tree_chunks_[mode], tree_arrivals_.as<unsigned>(), dst, s);
     if (ev1) NTF_CUDA(cudaEventRecord(ev1, s));
   } else if (unit_tab_[mode].p) {  // a fast plan exists (tables are built only then)
     fast_mttkrp(t_->data.p, t_->dtype, v, dF, unit_tab_[mode].as<int>(), partial_.as<double>(), dst, ctx_->sms, s,

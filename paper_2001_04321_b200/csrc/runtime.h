@@ -76,8 +76,10 @@ class MttkrpEngine {
   int kernels_per_call(int mode) const;
   ModeView view(int mode) const;
   std::string describe(int mode) const;
-  // Dimension tree (NTF_RUN_DIMTREE, order >= 3, fast plan for the TTM):
-  // run(0) first forms Y = T x_{N-1} A_{N-1}, and blocks 0..N-2 contract Y.
+  // Dimension tree (NTF_RUN_DIMTREE, order >= 3, fast plans for the partials):
+  // run(0) first forms Y_L = T x_h A_h .. x_{N-1} A_{N-1} and blocks 0..h-1
+  // contract it; run(h) forms Y_R = T x_0 A_0 .. x_{h-1} A_{h-1} for blocks
+  // h..N-1 (h = N-1: Y_R is block N-1's MTTKRP, computed directly).
   bool tree() const { return tree_; }
 
  private:
@@ -92,10 +94,18 @@ class MttkrpEngine {
   DevBuf unit_tab_[kMaxOrder];   // fast-path unit tables (empty: generic kernel)
   long long maxrows_ = 0;
   bool tree_ = false;
-  ModeView ttm_view_{};          // 2-way view (prod_{n<N-1} I_n) x I_{N-1}
-  DevBuf ttm_tab_, ybuf_;        // its unit table; Y (local rows x r, FP64)
+  int split_ = 0;                // dimension-tree split h (blocks < h contract Y_L, the rest Y_R)
+  ModeView ttm_view_{};          // Y_L view: (prod_{n<h} I_n) x I_h x ... x I_{N-1}
+  DevBuf ttm_tab_, ybuf_;        // its unit table; Y_L (local rows x r, FP64)
+  ModeView ttmr_view_{};         // Y_R view (h < N-1): I_0 x ... x I_{h-1} x (prod_{n>=h} I_n)
+  DevBuf ttmr_tab_, yrbuf_;      // its unit table; Y_R (partial over the local slab, FP64)
+  int order_ = 0;
+  int last_mode_ = -1;           // previous run() block (a tree partial is reused only in sweep order)
+  bool tree_mode(int mode) const { return tree_ && (mode < split_ || split_ < order_ - 1); }
   DevBuf counter_;               // arrival counter of the in-kernel split-K reduction
   int tree_chunks_[kMaxOrder] = {};
+  int tree_tiles_max_ = 1;
+  DevBuf tree_arrivals_;         // per-tile arrival counters of the tree kernel (self-resetting)
   TreeView tree_view(int mode) const;
 };
 

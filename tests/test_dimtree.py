@@ -1,7 +1,10 @@
 """Dimension-tree MTTKRP reuse (NTF_RUN_DIMTREE).
 
-Blocks 0..N-2 of an outer iteration contract Y = T x_{N-1} A_{N-1} instead of
-the tensor; results differ from the direct MTTKRPs only by summation order,
+With split h, blocks 0..h-1 of an outer iteration contract
+Y_L = T x_h A_h .. x_{N-1} A_{N-1} and blocks h..N-1 contract
+Y_R = T x_0 A_0 .. x_{h-1} A_{h-1} instead of the tensor (default h = N-1
+for 3-way, h = N/2 from 4-way; NTF_TREE_SPLIT overrides). Results differ
+from the direct MTTKRPs only by summation order,
 so the traces must meet the same parity bars against the oracle
 (parity.compare_traces: f_k within 1e-8 relative + the cancellation floor,
 identical restart decisions), for HER and AO, 3-way and 4-way.
@@ -34,6 +37,23 @@ def test_dimtree_her_trace_parity(P, oracle, shape, rank, sigma, seed):
     stats = compare_traces(trace, f0, recs, oracle.norm_sq(np.asarray(t)))
     assert stats["checked"] == 50
     assert model.is_nonnegative()
+
+
+@pytest.mark.parametrize("split", [1, 2, 3])
+@pytest.mark.parametrize("shape,rank,sigma,seed", [([20, 18, 16, 16], 6, 0.01, 103), ([64, 40, 48], 20, 0.001, 5)])
+def test_dimtree_every_split_her_parity(P, oracle, monkeypatch, shape, rank, sigma, seed, split):
+    """Every split point h of the tree (Y_L with merged rows and shifted
+    factors, Y_R with factor-offset tree contractions) meets the trace bars."""
+    if split >= len(shape):
+        pytest.skip("split must be < N")
+    monkeypatch.setenv("NTF_TREE_SPLIT", str(split))
+    t, truth, init = _instance(P, shape, rank, sigma, seed)
+    prov = P.GpuDenseProvider(t)
+    model, trace = P.her_run(prov, init, P.AoConfig(max_outer_iters=30, flags=P.RUN_DIMTREE), P.HerParams())
+    fo, f0, recs = oracle.run("her", np.asarray(t), init.factors, max_outer_iters=30)
+    stats = compare_traces(trace, f0, recs, oracle.norm_sq(np.asarray(t)))
+    assert stats["checked"] == 30
+    prov.close()
 
 
 @pytest.mark.parametrize("shape,rank,sigma,seed", CASES[:3])

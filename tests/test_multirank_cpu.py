@@ -12,10 +12,12 @@ The result must equal the single-process MTTKRP of the full tensor, and
 ||T||^2 must equal the all-reduced slab norms. The algebra is evaluated with
 the oracle (test infrastructure) on each slab; the collectives are gloo.
 
-With the dimension tree (NTF_RUN_DIMTREE) each rank contracts its slab with
-A_{N-1} first (Y_slab = T_slab x_{N-1} A_{N-1}, kernels_tree.cu) and forms
-blocks 0..N-2 from Y_slab; the exchange is the same (mode 1 gathered, the
-others all-reduced), so the same equality must hold.
+With the dimension tree (NTF_RUN_DIMTREE, split h) each rank contracts its
+slab into Y_L = T_slab x_h A_h .. x_{N-1} A_{N-1} (local rows) and
+Y_R = T_slab x_0 A_0 .. x_{h-1} A_{h-1} (a partial sum over the slab) and
+forms the blocks from them (kernels_tree.cu); the exchange is the same
+(mode 1 gathered, the others all-reduced, by linearity in Y_R), so the same
+equality must hold for every split.
 """
 import os
 
@@ -35,23 +37,32 @@ def _slab_mttkrp(oracle, t_slab, model, row0, mode):
     return oracle.mttkrp(t_slab, local, mode)
 
 
-def _slab_tree_mttkrp(t_slab, model, row0, mode):
-    """Block `mode` (< N-1) of one slab through Y_slab = T_slab x_{N-1} A_{N-1}."""
+def _slab_tree_mttkrp(t_slab, model, row0, mode, split):
+    """Block `mode` of one slab through the split dimension tree (runtime.cpp
+    MttkrpEngine): blocks < h contract Y_L = T_slab x_h A_h .. x_{N-1} A_{N-1},
+    blocks >= h contract Y_R = T_slab x_0 A_0(slab rows) .. x_{h-1} A_{h-1};
+    with h = N-1, block N-1 is the direct slab MTTKRP."""
     n = t_slab.ndim
     local = [a for a in model]
     local[0] = model[0][row0:row0 + t_slab.shape[0]]
-    y = np.tensordot(t_slab, local[n - 1], axes=([n - 1], [0]))  # (I_0..I_{N-2}, r)
-    letters = "abcdefg"[: n - 1]
-    ops = [y]
-    subs = [letters + "z"]
-    for j in range(n - 1):
+    letters = "abcdefg"[:n]
+    lo, hi = (0, split) if mode < split else (split, n)
+    # contract the other side of the split first
+    ops, subs = [t_slab], [letters]
+    for j in range(n):
+        if not lo <= j < hi:
+            ops.append(local[j])
+            subs.append(letters[j] + "z")
+    y = np.einsum(",".join(subs) + "->" + letters[lo:hi] + "z", *ops)
+    ops, subs = [y], [letters[lo:hi] + "z"]
+    for j in range(lo, hi):
         if j != mode:
             ops.append(local[j])
             subs.append(letters[j] + "z")
     return np.einsum(",".join(subs) + "->" + letters[mode] + "z", *ops)
 
 
-def _worker(rank, world, port, shape, rank_r, q, tree=False):
+def _worker(rank, world, port, shape, rank_r, q, split=0):
     import sys
     sys.path[:0] = [ROOT, os.path.join(ROOT, "oracle")]
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -69,8 +80,8 @@ def _worker(rank, world, port, shape, rank_r, q, tree=False):
         maxrows = max(P.slab_range(shape[0], p, world)[1] - P.slab_range(shape[0], p, world)[0]
                       for p in range(world))
         for mode in range(len(shape)):
-            if tree and mode < len(shape) - 1:
-                part = _slab_tree_mttkrp(slab, model, b, mode)
+            if split:
+                part = _slab_tree_mttkrp(slab, model, b, mode, split)
             else:
                 part = _slab_mttkrp(O, slab, model, b, mode)
             if mode == 0:
@@ -92,13 +103,15 @@ def _worker(rank, world, port, shape, rank_r, q, tree=False):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("tree", [False, True], ids=["direct", "dimtree"])
+@pytest.mark.parametrize("split", [0, 1, 2, 3], ids=["direct", "tree-h1", "tree-h2", "tree-h3"])
 @pytest.mark.parametrize("shape", [[7, 6, 5], [9, 4, 3, 5]])
-def test_slab_sharded_mttkrp_world2(shape, tree):
+def test_slab_sharded_mttkrp_world2(shape, split):
+    if split >= len(shape):
+        pytest.skip("split must be < N")
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    port = 29500 + (os.getpid() % 1000) + len(shape) + (10 if tree else 0)
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, shape, 3, q, tree)) for r in range(2)]
+    port = 29500 + (os.getpid() % 1000) + len(shape) + 10 * split
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, shape, 3, q, split)) for r in range(2)]
     for p in procs:
         p.start()
     results = dict(q.get(timeout=120) for _ in procs)
