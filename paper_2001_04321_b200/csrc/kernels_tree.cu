@@ -156,8 +156,10 @@ int tree_tiles(const TreeView& v) { return int((v.I * v.rank + kTreeTile - 1) / 
 int tree_chunks(const TreeView& v, int sms) {
   const long long tiles = tree_tiles(v);
   const long long Q = v.L * v.R;
-  // about two CTAs per SM over the whole grid
-  long long chunks = (2LL * sms + tiles - 1) / tiles;
+  // at most two CTAs per SM over the whole grid (two are resident at 92
+  // registers x 256 threads): one wave, no tail (r01e at C2: 24 tiles x 13
+  // chunks = 312 CTAs ran a 16-CTA second wave, 17 us per launch)
+  long long chunks = std::max(1LL, (2LL * sms) / tiles);
   // a chunk's Khatri-Rao rows live in shared memory (<= 192 KB)
   const long long min_chunks = (Q * v.rank * (long long)sizeof(double) + 192 * 1024 - 1) / (192 * 1024);
   chunks = std::max(1LL, std::min(std::max(chunks, min_chunks), Q));

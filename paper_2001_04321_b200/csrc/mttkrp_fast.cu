@@ -37,6 +37,7 @@ struct Choice {
   fast::Params p;
   int layout, grid, threads;
   size_t smem;
+  bool mma = false;  // FP64 DMMA consumers
 };
 
 bool choose(const ModeView& v, int dtype, int sms, Choice* out) {
@@ -139,6 +140,15 @@ bool choose(const ModeView& v, int dtype, int sms, Choice* out) {
     out->smem = size_t(p.stages) * per_stage + 3 * size_t(p.stages) * sizeof(uint64_t);
     out->cfg = cfg;
     out->layout = layout;
+    // FP64: DMMA consumers when the blocking has them and their fragment
+    // scratch fits the stage buffers (NTF_FAST_MMA=0: DFMA consumers)
+    {
+      const char* me = std::getenv("NTF_FAST_MMA");
+      const bool want = !(me && std::atoi(me) == 0);
+      const fast::LaunchFn mf = layout == fast::kRow ? cfg.row_mma : cfg.col_mma;
+      const size_t scr = size_t(MW) * KW * fast::mma_scratch_doubles(cfg.G, cfg.B, cfg.A) * sizeof(double);
+      out->mma = want && mf && dtype == NTF_DTYPE_F64 && scr <= size_t(p.stages) * p.t_stage_bytes;
+    }
     return true;
   }
   return false;
@@ -321,7 +331,8 @@ void fast_mttkrp(const void* t, int dtype, const ModeView& v, const DevFactors* 
     NTF_CUDA(cudaMemsetAsync(prof, 0, n * sizeof(unsigned long long), s));
     ch.p.prof = prof;
   }
-  fast::LaunchFn fn = ch.layout == fast::kRow ? ch.cfg.row : ch.cfg.col;
+  fast::LaunchFn fn = ch.layout == fast::kRow ? (ch.mma ? ch.cfg.row_mma : ch.cfg.row)
+                                              : (ch.mma ? ch.cfg.col_mma : ch.cfg.col);
   fn(map, ch.p, ch.grid, ch.threads, ch.smem, s);
   if (profiling) {
     std::vector<unsigned long long> h(size_t(ch.grid) * fast::kProfSlots);
@@ -366,8 +377,8 @@ std::string fast_mttkrp_describe(const ModeView& v, int dtype, int sms) {
   Choice ch;
   if (!choose(v, dtype, sms, &ch)) return "generic";
   char buf[256];
-  snprintf(buf, sizeof buf, "%s G=%d B=%d A=%d MW=%d KW=%d m_cta=%d stages=%d grid=%d threads=%d smem=%zu units=%lld",
-           ch.layout == fast::kRow ? "row" : "col", ch.cfg.G, ch.cfg.B, ch.cfg.A, ch.p.MW, ch.p.KW, ch.p.m_cta,
+  snprintf(buf, sizeof buf, "%s%s G=%d B=%d A=%d MW=%d KW=%d m_cta=%d stages=%d grid=%d threads=%d smem=%zu units=%lld",
+           ch.layout == fast::kRow ? "row" : "col", ch.mma ? "+dmma" : "", ch.cfg.G, ch.cfg.B, ch.cfg.A, ch.p.MW, ch.p.KW, ch.p.m_cta,
            ch.p.stages, ch.grid, ch.threads, ch.smem, ch.p.units);
   return buf;
 }

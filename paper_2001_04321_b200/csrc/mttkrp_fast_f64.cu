@@ -25,7 +25,18 @@ void launch_impl(const CUtensorMap& map, const Params& p, int grid, int threads,
   NTF_CUDA(cudaLaunchKernelEx(&cfg, fn, map, p));
 }
 
-#define NTF_CFG(T, G, B, A) KernelCfg{G, B, A, launch_impl<T, G, B, A, kRow>, launch_impl<T, G, B, A, kCol>}
+// DMMA consumers exist for blockings whose warp rows form 8-row fragments
+template <typename T, int G, int B, int A, int L>
+constexpr LaunchFn mma_launch() {
+  if constexpr (((32 / G) * A) % 8 == 0)
+    return launch_impl<T, G, B, A, L>;
+  else
+    return nullptr;
+}
+
+#define NTF_CFG(T, G, B, A)                                                                          \
+  KernelCfg{G, B, A, launch_impl<T, G, B, A, kRow>, launch_impl<T, G, B, A, kCol>, 4,                 \
+            mma_launch<T, G, B, A, kRowMma>(), mma_launch<T, G, B, A, kColMma>()}
 
 // Blocking per rank. Shared-memory bytes per DFMA are 8 (A + B) / (A B)
 // (T and W values delivered per lane), and the SM moves 128 B/clk against 64

@@ -109,8 +109,20 @@ __device__ __forceinline__ const float* factor_ptr<float>(const DevFactors* F, i
 
 // G column groups of B columns each (padded to BP so 16-byte loads stay
 // aligned); RG = 32/G row groups; A rows per lane.
+// FP64 tensor-core step (DMMA): D[8x8] += A[8x4] B[4x8]; lane (g, t) holds
+// A[g][t], B[t][g] and D[g][2t], D[g][2t+1] (g = lane / 4, t = lane % 4).
+__device__ __forceinline__ void dmma_8x8x4(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
+
+// LAYOUT: kRow / kCol with CUDA-core FMAs; kRowMma / kColMma (FP64 only):
+// the consumers run the same stages through DMMA (see the consumer loop).
 template <typename T, int G, int B, int A, int LAYOUT>
 __global__ void __launch_bounds__(max_threads_es(A, B, int(sizeof(T))), 1) mttkrp_fast_kernel(const __grid_constant__ CUtensorMap tmap, Params p) {
+  constexpr bool MMA = LAYOUT >= kRowMma;
+  constexpr int LAY = LAYOUT & 1;
   using VT = Vec<T>;
   using V = typename VT::V;
   constexpr int VEC = VT::N;
@@ -237,7 +249,7 @@ __global__ void __launch_bounds__(max_threads_es(A, B, int(sizeof(T))), 1) mttkr
         mbar_expect_tx(&full[s], p.tx_bytes);
         for (int mb = 0; mb < p.n_mbox; ++mb) {
           const int m0 = mt * p.m_cta + mb * p.m_box;
-          if (LAYOUT == kRow)
+          if (LAY == kRow)
             tma_load_3d(ts + size_t(mb) * p.m_box * 128, &tmap, &full[s], e[0], m0, e[1]);
           else
             tma_load_3d(ts + size_t(mb) * p.m_box * p.kbox * sizeof(T), &tmap, &full[s], m0, e[0], 0);
@@ -330,7 +342,7 @@ __global__ void __launch_bounds__(max_threads_es(A, B, int(sizeof(T))), 1) mttkr
     // rows (one 16-byte read), the last A % VEC rows one by one.
     constexpr int AV = (A / VEC) * VEC;
     auto lane_row = [&](int i) {
-      if (LAYOUT == kRow) return mw * RW + rg + RG * i;
+      if (LAY == kRow) return mw * RW + rg + RG * i;
       if (i < AV) return mw * RW + VEC * rg + (i % VEC) + VEC * RG * (i / VEC);
       return mw * RW + VEC * RG * (A / VEC) + rg + RG * (i - AV);
     };
@@ -339,7 +351,7 @@ __global__ void __launch_bounds__(max_threads_es(A, B, int(sizeof(T))), 1) mttkr
 #pragma unroll
     for (int i = 0; i < A; ++i) {
       const int m = lane_row(i);
-      if (LAYOUT == kRow)
+      if (LAY == kRow)
         off[i] = m;  // row index; byte offset m*128, swizzle key m & 7
       else
         off[i] = (m / p.m_box) * p.m_box * p.kbox + (m % p.m_box);  // element offset at k = 0
@@ -373,6 +385,87 @@ __global__ void __launch_bounds__(max_threads_es(A, B, int(sizeof(T))), 1) mttkr
     uint32_t phase = 0;
     long long cw_full = 0;
     const long long ct0 = prof_on ? clock64() : 0;
+    if constexpr (MMA) {
+      // ---- FP64 DMMA consumer. The warp's RW rows are NMF 8-row fragments,
+      // the G*B columns NNF 8-column fragments; per 4-k step a lane loads one
+      // T value per row fragment and one W value per column fragment for
+      // NMF*NNF DMMAs (256 FMAs each): ~1/10 of the shared-memory operand
+      // traffic per FMA of the register-blocked DFMA loop, which is bound by
+      // that traffic (128 B/clk/SM against 64 DFMA/clk). ROW fragments take
+      // rows with swizzle keys (m & 7) = 0,2,4,6 | 1,3,5,7 on the two
+      // half-warps so the 16-byte chunks of a k pair never share banks.
+      constexpr int RWc = RG * A;
+      constexpr int NMF = RWc / 8;
+      constexpr int NNF = (G * B + 7) / 8;
+      static_assert(RWc % 8 == 0, "DMMA consumer needs 8-row fragments");
+      const int g8 = lane >> 2, t4 = lane & 3;
+      const int frow = LAY == kRow ? (((g8 & 3) << 1) | (g8 >> 2)) : g8;
+      int wcol[NNF];
+#pragma unroll
+      for (int jn = 0; jn < NNF; ++jn) {
+        const int c = 8 * jn + g8;
+        wcol[jn] = c < G * B ? (c / B) * BP + c % B : 0;  // padded columns: any finite column, discarded
+      }
+      int moff[NMF];
+#pragma unroll
+      for (int f = 0; f < NMF; ++f) {
+        const int m = mw * RWc + 8 * f + frow;
+        moff[f] = LAY == kRow ? m : (m / p.m_box) * p.m_box * p.kbox + (m % p.m_box);
+      }
+      double dacc[NMF][NNF][2];
+#pragma unroll
+      for (int f = 0; f < NMF; ++f)
+#pragma unroll
+        for (int jn = 0; jn < NNF; ++jn) dacc[f][jn][0] = dacc[f][jn][1] = 0.0;
+      const int ksteps = p.kbox / 4;
+      for (long long u = u0; u < u1; ++u) {
+        mbar_wait(&full[s], phase);
+        const unsigned char* ts = t_base + size_t(s) * p.t_stage_bytes;
+        const double* wsd = reinterpret_cast<const double*>(w_base) + size_t(s) * (p.w_stage_bytes / sizeof(double));
+        for (int ks = kw; ks < ksteps; ks += p.KW) {
+          const int k = 4 * ks + t4;
+          double bv[NNF];
+#pragma unroll
+          for (int jn = 0; jn < NNF; ++jn) bv[jn] = wsd[k * p.wld + wcol[jn]];
+#pragma unroll
+          for (int f = 0; f < NMF; ++f) {
+            double av;
+            if (LAY == kRow) {
+              const int m = moff[f];
+              av = *reinterpret_cast<const double*>(ts + m * 128 + ((((k >> 1) ^ m) & 7) << 4) + ((k & 1) << 3));
+            } else {
+              av = reinterpret_cast<const double*>(ts)[moff[f] + k * p.m_box];
+            }
+#pragma unroll
+            for (int jn = 0; jn < NNF; ++jn) dmma_8x8x4(dacc[f][jn], av, bv[jn]);
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+        if (++s == stages) {
+          s = 0;
+          phase ^= 1;
+        }
+      }
+      // fragments -> the (rg, cg) register layout of the epilogue, through a
+      // per-warp scratch in the idle stage buffers (every consumer is past
+      // its last stage read after the barrier; the host checks the size)
+      constexpr int LDS = NNF * 8 + 1;
+      asm volatile("bar.sync 1, %0;" ::"r"(n_consumers * 32) : "memory");
+      double* scr = reinterpret_cast<double*>(smem) + size_t(cw) * RWc * LDS;
+#pragma unroll
+      for (int f = 0; f < NMF; ++f)
+#pragma unroll
+        for (int jn = 0; jn < NNF; ++jn) {
+          scr[(8 * f + frow) * LDS + 8 * jn + 2 * t4] = dacc[f][jn][0];
+          scr[(8 * f + frow) * LDS + 8 * jn + 2 * t4 + 1] = dacc[f][jn][1];
+        }
+      __syncwarp();
+#pragma unroll
+      for (int i = 0; i < A; ++i)
+#pragma unroll
+        for (int b = 0; b < B; ++b) acc[i][b] = T(scr[(lane_row(i) - mw * RWc) * LDS + cg * B + b]);
+    } else
     for (long long u = u0; u < u1; ++u) {
       {
         const long long t0 = prof_on ? clock64() : 0;
@@ -381,7 +474,7 @@ __global__ void __launch_bounds__(max_threads_es(A, B, int(sizeof(T))), 1) mttkr
       }
       const unsigned char* ts = t_base + size_t(s) * p.t_stage_bytes;
       const T* ws = w_base + size_t(s) * (p.w_stage_bytes / sizeof(T)) + cg * BP;
-      if (LAYOUT == kRow) {
+      if (LAY == kRow) {
         constexpr int KCH = 128 / 16;  // 16-byte chunks per 128-byte row
         for (int pc = kw; pc < KCH; pc += p.KW) {
           // Shared-memory bandwidth (128 B/clk/SM, every lane receiving its

@@ -10,7 +10,9 @@
 namespace ntfb {
 namespace fast {
 
-enum { kRow = 0, kCol = 1 };
+enum { kRow = 0, kCol = 1, kRowMma = 2, kColMma = 3 };
+// DMMA consumer scratch per warp (doubles): rows x (8 * column fragments + 1)
+constexpr int mma_scratch_doubles(int G, int B, int A) { return (32 / G) * A * (((G * B + 7) / 8) * 8 + 1); }
 
 // Unit table: per unit, ints
 //   [0] ROW: rho0 / COL: l0 (TMA coordinate along the reduction)
@@ -60,7 +62,8 @@ using LaunchFn = void (*)(const CUtensorMap& map, const Params& p, int grid, int
 struct KernelCfg {
   int G, B, A;
   LaunchFn row, col;
-  int cons = 4;  // target consumer warps per CTA (8: two per SM sub-partition)
+  int cons = 4;
+  LaunchFn row_mma = nullptr, col_mma = nullptr;  // FP64 DMMA consumers (null: none)  // target consumer warps per CTA (8: two per SM sub-partition)
 };
 
 // Thread cap of an instantiation: small accumulator tiles allow 16 warps

@@ -1,5 +1,6 @@
-timeout 600 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
-export NTF_B200_LIB=$PWD/build/prof/libntf_b200_prof.so
-for c in c2 c3 c4; do python tools/tune.py $c 10 2>&1 | grep -E "nnls \(|row loop"; done
-unset NTF_B200_LIB
-for c in c2 c3; do timeout 300 python bench.py --config $c --no-cpu-baseline 2>&1 | tail -1 | python3 -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['config']['workload'][:20], round(d['value'],1), d['roofline']['per_mode_ms'])"; done
+# full ncu captures: tree kernel and NNLS kernel (C2), Y_R COL pass (C3)
+mkdir -p gpurun_out/p24
+timeout 600 ncu --set full --import-source on --clock-control none -k regex:tree_mttkrp -s 4 -c 1 -o gpurun_out/p24/tree_c2 python bench.py --config c2 --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/p24/ncu_tree.log 2>&1
+timeout 600 ncu --set full --import-source on --clock-control none -k regex:nnls_stream -s 6 -c 1 -o gpurun_out/p24/nnls_c2 python bench.py --config c2 --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/p24/ncu_nnls.log 2>&1
+timeout 600 ncu --set full --import-source on --clock-control none -k regex:mttkrp_fast -s 2 -c 2 -o gpurun_out/p24/fast_c3 python bench.py --config c3 --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/p24/ncu_fast.log 2>&1
+echo done
