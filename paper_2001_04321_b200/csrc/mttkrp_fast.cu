@@ -85,6 +85,10 @@ bool choose(const ModeView& v, int dtype, int sms, Choice* out) {
   }
   // Tall views (the dimension tree's T x_N A_N has I = prod_{n<N-1} I_n rows)
   // need smaller m-tiles for a pipeline of >= 2 NP stages: fewer m-warps.
+  // FP64: DMMA consumers when the blocking has them (NTF_FAST_MMA=0: DFMA)
+  const char* mma_env = std::getenv("NTF_FAST_MMA");
+  const bool mma_try = !(mma_env && std::atoi(mma_env) == 0) && dtype == NTF_DTYPE_F64 &&
+                       (layout == fast::kRow ? cfg.row_mma : cfg.col_mma) != nullptr;
   for (int MW = MW0; MW >= 1; --MW) {
     const int n_mtiles = MW == MW0 ? n_mtiles0 : int((v.I + (long long)MW * RW - 1) / ((long long)MW * RW));
     // at least four consumer warps (one per SM sub-partition): split k
@@ -111,12 +115,14 @@ bool choose(const ModeView& v, int dtype, int sms, Choice* out) {
       p.kbox = int(128 / es);
       p.nbox_r = (v.R + p.kbox - 1) / p.kbox;
       p.units = v.L * p.nbox_r;
+      p.m_pitch = p.m_box;
       p.t_stage_bytes = unsigned(m_cta * 128);
     } else {
       p.kbox = int(128 / es);  // 16 doubles / 32 floats of l per unit
       p.nbox_r = 0;
       p.units = (v.L + p.kbox - 1) / p.kbox;
-      p.t_stage_bytes = unsigned(size_t(m_cta) * p.kbox * es);
+      p.m_pitch = (mma_try && p.m_box + 4 <= 256) ? p.m_box + 4 : p.m_box;
+      p.t_stage_bytes = unsigned(size_t(p.n_mbox) * p.m_pitch * p.kbox * es);
     }
     p.tx_bytes = p.t_stage_bytes;
     p.w_stage_bytes = unsigned((size_t(p.kbox) * p.wld * es + 127) / 128 * 128);
@@ -143,11 +149,8 @@ bool choose(const ModeView& v, int dtype, int sms, Choice* out) {
     // FP64: DMMA consumers when the blocking has them and their fragment
     // scratch fits the stage buffers (NTF_FAST_MMA=0: DFMA consumers)
     {
-      const char* me = std::getenv("NTF_FAST_MMA");
-      const bool want = !(me && std::atoi(me) == 0);
-      const fast::LaunchFn mf = layout == fast::kRow ? cfg.row_mma : cfg.col_mma;
       const size_t scr = size_t(MW) * KW * fast::mma_scratch_doubles(cfg.G, cfg.B, cfg.A) * sizeof(double);
-      out->mma = want && mf && dtype == NTF_DTYPE_F64 && scr <= size_t(p.stages) * p.t_stage_bytes;
+      out->mma = mma_try && scr <= size_t(p.stages) * p.t_stage_bytes;
     }
     return true;
   }
@@ -177,7 +180,7 @@ void make_map(const void* t, int dtype, const ModeView& v, const Choice& ch, CUt
     dims[2] = 1;
     strides[0] = cuuint64_t(v.I * es);
     strides[1] = cuuint64_t(v.I * v.L * es);
-    box[0] = cuuint32_t(ch.p.m_box);
+    box[0] = cuuint32_t(ch.p.m_pitch);
     box[1] = cuuint32_t(ch.p.kbox);
     box[2] = 1;
     sw = CU_TENSOR_MAP_SWIZZLE_NONE;

@@ -252,7 +252,7 @@ __global__ void __launch_bounds__(max_threads_es(A, B, int(sizeof(T))), 1) mttkr
           if (LAY == kRow)
             tma_load_3d(ts + size_t(mb) * p.m_box * 128, &tmap, &full[s], e[0], m0, e[1]);
           else
-            tma_load_3d(ts + size_t(mb) * p.m_box * p.kbox * sizeof(T), &tmap, &full[s], m0, e[0], 0);
+            tma_load_3d(ts + size_t(mb) * p.m_pitch * p.kbox * sizeof(T), &tmap, &full[s], m0, e[0], 0);
         }
         T* aq = aq_of(s);
         int* info = info_of(s);
@@ -354,7 +354,7 @@ __global__ void __launch_bounds__(max_threads_es(A, B, int(sizeof(T))), 1) mttkr
       if (LAY == kRow)
         off[i] = m;  // row index; byte offset m*128, swizzle key m & 7
       else
-        off[i] = (m / p.m_box) * p.m_box * p.kbox + (m % p.m_box);  // element offset at k = 0
+        off[i] = (m / p.m_box) * p.m_pitch * p.kbox + (m % p.m_box);  // element offset at k = 0
     }
     // periodic FP64 flush of the FP32 accumulators (KW == 1: each output
     // entry of the CTA belongs to exactly one lane, so no race)
@@ -410,7 +410,7 @@ __global__ void __launch_bounds__(max_threads_es(A, B, int(sizeof(T))), 1) mttkr
 #pragma unroll
       for (int f = 0; f < NMF; ++f) {
         const int m = mw * RWc + 8 * f + frow;
-        moff[f] = LAY == kRow ? m : (m / p.m_box) * p.m_box * p.kbox + (m % p.m_box);
+        moff[f] = LAY == kRow ? m : (m / p.m_box) * p.m_pitch * p.kbox + (m % p.m_box);
       }
       double dacc[NMF][NNF][2];
 #pragma unroll
@@ -434,7 +434,7 @@ __global__ void __launch_bounds__(max_threads_es(A, B, int(sizeof(T))), 1) mttkr
               const int m = moff[f];
               av = *reinterpret_cast<const double*>(ts + m * 128 + ((((k >> 1) ^ m) & 7) << 4) + ((k & 1) << 3));
             } else {
-              av = reinterpret_cast<const double*>(ts)[moff[f] + k * p.m_box];
+              av = reinterpret_cast<const double*>(ts)[moff[f] + k * p.m_pitch];
             }
 #pragma unroll
             for (int jn = 0; jn < NNF; ++jn) dmma_8x8x4(dacc[f][jn], av, bv[jn]);
@@ -515,7 +515,7 @@ __global__ void __launch_bounds__(max_threads_es(A, B, int(sizeof(T))), 1) mttkr
           }
 #pragma unroll
           for (int i4 = 0; i4 < A / VEC; ++i4) {
-            const V tv = *reinterpret_cast<const V*>(tt + off[i4 * VEC] + k * p.m_box);
+            const V tv = *reinterpret_cast<const V*>(tt + off[i4 * VEC] + k * p.m_pitch);
 #pragma unroll
             for (int e = 0; e < VEC; ++e) {
               const T t = VT::get(tv, e);
@@ -525,7 +525,7 @@ __global__ void __launch_bounds__(max_threads_es(A, B, int(sizeof(T))), 1) mttkr
           }
 #pragma unroll
           for (int i = AV; i < A; ++i) {
-            const T t = tt[off[i] + k * p.m_box];
+            const T t = tt[off[i] + k * p.m_pitch];
 #pragma unroll
             for (int b = 0; b < B; ++b) acc[i][b] = fma(t, w[b], acc[i][b]);
           }

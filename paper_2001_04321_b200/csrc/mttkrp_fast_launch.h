@@ -42,6 +42,10 @@ struct Params {
   long long nbox_r; // ROW: rho boxes per l
   int kbox;         // reduction indices per unit
   int m_box, n_mbox, m_cta, ctas_per_mtile;
+  // COL: shared-memory row pitch of a box (>= m_box); the DMMA consumers
+  // read 4 k rows per half-warp, so the pitch is m_box + 4 doubles (32 B off
+  // a bank period; the 4 extra rows are real neighbouring rows, unused)
+  int m_pitch;
   int MW, KW, NP, stages, wld;  // consumer m-warps, k-warps, producer warps
   unsigned t_stage_bytes, w_stage_bytes, aq_stage_bytes, tx_bytes;
   const int* utab;       // units x kUnitInts (device)
