@@ -60,7 +60,8 @@ typedef struct {
 } ntf_inner_stop;
 
 /* Performance options of the GPU drivers (no reference counterpart). */
-#define NTF_RUN_DIMTREE 1u  /* reuse T x_N A_N across the modes of a sweep   */
+#define NTF_RUN_DIMTREE 1u  /* dimension tree: two partial contractions per
+                               sweep (Y_L, Y_R) instead of N full passes    */
 #define NTF_RUN_NO_GRAPH 2u /* launch kernels directly instead of a CUDA graph */
 #define NTF_RUN_GENERIC 4u  /* force the generic MTTKRP kernel (testing)     */
 

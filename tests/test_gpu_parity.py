@@ -57,6 +57,22 @@ def test_mttkrp_medium_f64(P, oracle, shape, rank):
         assert rel_fro(prov.mttkrp(m, mode), oracle.mttkrp(t, m, mode)) < 1e-12
 
 
+@pytest.mark.parametrize("mma", ["1", "0"], ids=["dmma", "dfma"])
+@pytest.mark.parametrize("shape,rank", [([300, 30, 30], 20), ([64, 48, 32], 32), ([20, 21, 22, 23], 16),
+                                        ([40, 30, 20], 64), ([96, 40, 50], 8)])
+def test_mttkrp_f64_consumer_kinds(P, oracle, monkeypatch, shape, rank, mma):
+    """FP64 fast MTTKRP with DMMA consumers (default) and with the DFMA
+    register tiles (NTF_FAST_MMA=0), ROW and COL views, 1e-12 vs the oracle."""
+    monkeypatch.setenv("NTF_FAST_MMA", mma)
+    gen = np.random.default_rng(7 * sum(shape) + rank)
+    t = gen.random(shape)
+    m = [gen.random((d, rank)) for d in shape]
+    prov = P.GpuDenseProvider(t)
+    for mode in range(len(shape)):
+        assert rel_fro(prov.mttkrp(m, mode), oracle.mttkrp(t, m, mode)) < 1e-12
+    prov.close()
+
+
 @pytest.mark.parametrize("shape,rank", [([50, 50, 50], 10), ([60, 50, 40], 32), ([30, 20, 40], 64)])
 def test_mttkrp_f32(P, oracle, shape, rank):
     gen = np.random.default_rng(3 + rank)
