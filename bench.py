@@ -54,6 +54,15 @@ METRIC = "HER-AHALS outer iters/s"
 UNIT = "iters/s"
 
 
+def tree_split(order):
+    """Dimension-tree split h of the runtime (runtime.cpp MttkrpEngine):
+    N-1 for 3-way tensors, N/2 from 4-way; NTF_TREE_SPLIT overrides."""
+    h = order // 2 if order >= 4 else order - 1
+    if os.environ.get("NTF_TREE_SPLIT"):
+        h = max(1, min(order - 1, int(os.environ["NTF_TREE_SPLIT"])))
+    return h
+
+
 def _peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -239,11 +248,14 @@ def run_ours(args):
     trace = sess.trace()
     n_modes = len(shape)
     per_mode_ms = [kms[i] / max(kcnt[i], 1) for i in range(n_modes)]
-    # the roofline kernel is a full MTTKRP pass: every mode without the
-    # dimension tree; with it only block N-1 is one (blocks 0..N-2 contract
-    # Y, block 0 after the T x_{N-1} A_{N-1} pass) -- per_mode_ms shows all
+    # the roofline kernel is a full MTTKRP pass over the tensor: every mode
+    # without the dimension tree; with it the two passes of an iteration,
+    # Y_L (timed at block 0) and Y_R (block h; h = N-1 for 3-way: block N-1's
+    # own MTTKRP), each timed alone -- the other blocks' per_mode_ms are their
+    # tree contractions
+    split = tree_split(len(shape))
     if args.dimtree:
-        avg_ms = per_mode_ms[-1]
+        avg_ms = (per_mode_ms[0] + per_mode_ms[split]) / 2
     else:
         avg_ms = sum(kms) / max(sum(kcnt), 1)
     local_shape = list(t_local.shape)
@@ -302,7 +314,7 @@ def run_ours(args):
             "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm_peak, "unit": "GB/s",
                          "frac": achieved_gbs / hbm_peak, "traffic": traffic, "peak_kind": peak_kind,
                          "traffic_source": "profiles/traffic.json (ncu dram__bytes_read+write per launch)",
-                         "kernel": ("MTTKRP full pass of block N-1 (dimension tree on)" if args.dimtree
+                         "kernel": (f"MTTKRP full tensor passes (Y_L at block 0, Y_R at block {split}; dimension tree on)" if args.dimtree
                                     else "MTTKRP (main kernel, avg over modes)"),
                          "bytes_per_launch": bytes_per, "avg_launch_ms": avg_ms,
                          "per_mode_ms": per_mode_ms,

@@ -53,7 +53,12 @@ bool lookup_f64(int r, long long rows, KernelCfg* out) {
   else if (r <= 8) *out = NTF_CFG(double, 2, 4, 4);
   else if (r <= 10) *out = NTF_CFG(double, 2, 5, 4);
   else if (r <= 12) *out = NTF_CFG(double, 2, 6, 6);
-  else if (r <= 16) *out = (rows > 64 && rows <= 112) ? NTF_CFG(double, 2, 8, 7) : NTF_CFG(double, 2, 8, 8);
+  else if (r <= 16) {
+    *out = (rows > 64 && rows <= 112) ? NTF_CFG(double, 2, 8, 7) : NTF_CFG(double, 2, 8, 8);
+    // DMMA consumers (r01f sweep, C3): eight consumer warps, 1432 -> 1466 iters/s
+    const char* me = std::getenv("NTF_FAST_MMA");
+    if (!(me && std::atoi(me) == 0)) out->cons = 8;
+  }
   else if (r <= 20) {
     // measured (r01, C2): 8 consumer warps of 8 x 5 tiles beat 4 of 10 x 10
     // on every mode, and the COL layout most (80 vs 100 us)

@@ -280,15 +280,23 @@ void MttkrpEngine::run(int mode, const DevFactors* dF, double* out, cudaStream_t
     // A partial is formed by the first block of its side; a block reached
     // out of sweep order (the pivot objective's lone block N-1,
     // driver_common.hpp:50-56) forms it with the current factors.
-    if (mode == 0 || (mode < split_ && !seq))
+    // kernel timing (ev0/ev1): a block that forms a partial times that full
+    // tensor pass alone, the other blocks time their tree contraction
+    bool pass = false;
+    if (mode == 0 || (mode < split_ && !seq)) {
       fast_mttkrp(t_->data.p, t_->dtype, ttm_view_, dF, ttm_tab_.as<int>(), partial_.as<double>(), ybuf_.as<double>(),
                   ctx_->sms, s, counter_.as<unsigned>());
-    if (mode == split_ || (mode > split_ && !seq))
+      pass = true;
+    }
+    if (mode == split_ || (mode > split_ && !seq)) {
       fast_mttkrp(t_->data.p, t_->dtype, ttmr_view_, dF, ttmr_tab_.as<int>(), partial_.as<double>(),
                   yrbuf_.as<double>(), ctx_->sms, s, counter_.as<unsigned>());
+      pass = true;
+    }
+    if (ev1 && pass) NTF_CUDA(cudaEventRecord(ev1, s));
     launch_tree_mttkrp(mode < split_ ? ybuf_.as<double>() : yrbuf_.as<double>(), tree_view(mode), dF,
                        partial_.as<double>(), tree_chunks_[mode], tree_arrivals_.as<unsigned>(), dst, s);
-    if (ev1) NTF_CUDA(cudaEventRecord(ev1, s));
+    if (ev1 && !pass) NTF_CUDA(cudaEventRecord(ev1, s));
   } else if (unit_tab_[mode].p) {  // a fast plan exists (tables are built only then)
     fast_mttkrp(t_->data.p, t_->dtype, v, dF, unit_tab_[mode].as<int>(), partial_.as<double>(), dst, ctx_->sms, s,
                 counter_.as<unsigned>());
