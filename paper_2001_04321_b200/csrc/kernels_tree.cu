@@ -21,21 +21,33 @@
 // tree_mttkrp_kernel: CTA (chunk, tile) owns a contiguous range of the
 // flattened reduction index q = l * R' + rho and a tile of (i, c) output
 // pairs (one pair per thread, consecutive pairs on consecutive lanes); it
-// forms the chunk's Khatri-Rao rows in shared memory, streams Y with
-// kTreeQB loads in flight per thread and writes its partial to slot
-// [chunk][pair]. The last CTA of a tile to arrive (arrival counter per
-// tile, reset by that CTA, so graph replays need no memset) sums the slots
-// of the tile in chunk order: one launch per block, no atomics on data,
-// bit-reproducible.
+// forms the chunk's Khatri-Rao rows in shared memory and streams Y with
+// kTreeQB loads in flight per thread (the first batch before the factor
+// round trips). The chunks of a tile form one thread-block cluster (<= 8)
+// and sum their partials in chunk order over distributed shared memory.
+// Fallback when a chunk's Khatri-Rao rows exceed shared memory: more
+// chunks, partials in global slots, and the last CTA of a tile to arrive
+// (self-resetting arrival counter) sums them in chunk order. No atomics on
+// data either way: bit-reproducible.
+#include <cooperative_groups.h>
+
+#include <cstdlib>
+
 #include "ntf_internal.h"
 
 namespace ntfb {
 namespace {
 
+namespace cg = cooperative_groups;
+
 constexpr int kTreeThreads = 256;
 constexpr int kTreeTile = kTreeThreads;  // output pairs per CTA tile
 constexpr int kTreeQB = 16;              // q steps per load batch
 
+// CLUSTER: the chunks of a tile are one thread-block cluster (grid.x = the
+// cluster size); the chunk partials are summed in chunk order over
+// distributed shared memory, no global slots, fences or arrival counters.
+template <bool CLUSTER>
 __global__ void __launch_bounds__(kTreeThreads) tree_mttkrp_kernel(const double* __restrict__ Y, TreeView v,
                                                                    const DevFactors* __restrict__ F,
                                                                    double* __restrict__ partial, int qpc,
@@ -109,8 +121,8 @@ __global__ void __launch_bounds__(kTreeThreads) tree_mttkrp_kernel(const double*
   }
   __syncthreads();
 
+  double acc = 0.0;
   if (ok) {
-    double acc = 0.0;
     for (int q = q0; q < q1;) {
       const int n = min(kTreeQB, q1 - q);
       double ynext[kTreeQB];
@@ -122,7 +134,26 @@ __global__ void __launch_bounds__(kTreeThreads) tree_mttkrp_kernel(const double*
       for (int b = 0; b < kTreeQB; ++b) y[b] = ynext[b];
       q += n;
     }
-    partial[(long long)blockIdx.x * pairs + p] = acc;
+    if (!CLUSTER) partial[(long long)blockIdx.x * pairs + p] = acc;
+  }
+  if constexpr (CLUSTER) {
+    __shared__ double cpart[kTreeThreads];
+    cg::cluster_group cl = cg::this_cluster();
+    cpart[threadIdx.x] = acc;
+    cl.sync();
+    // CTA k of the cluster sums pairs [k*per, (k+1)*per) of the tile over
+    // the cluster's CTAs in rank (= chunk) order
+    const int ncl = int(cl.num_blocks()), me = int(cl.block_rank());
+    const int per = kTreeThreads / ncl;
+    if (int(threadIdx.x) < per) {
+      const int e = me * per + int(threadIdx.x);
+      double s = 0.0;
+      for (int c = 0; c < ncl; ++c) s += cl.map_shared_rank(cpart, c)[e];
+      const int pe = int(blockIdx.y) * kTreeTile + e;
+      if (pe < pairs) out[pe] = s;
+    }
+    cl.sync();  // no CTA leaves while another still reads its partials
+    return;
   }
 
   // last arrival of the tile sums the chunk slots in chunk order
@@ -171,15 +202,49 @@ void launch_tree_mttkrp(const double* Y, const TreeView& v, const DevFactors* dF
   const long long pairs = v.I * v.rank;
   const long long Q = v.L * v.R;
   if (Q >= (1LL << 31) || pairs >= (1LL << 31)) throw Unsupported("dimension tree: view too large for 32-bit indexing");
+  const int tiles = tree_tiles(v);
+  // cluster path: up to 8 chunks per tile, one wave of at most two CTAs per
+  // SM (NTF_TREE_ATOMIC=1: always the global-slot path)
+  {
+    int ncl = 8;
+    const int sms = device_sm_count();
+    while (ncl > 1 && (ncl > Q || (long long)tiles * ncl > 2LL * sms)) ncl /= 2;
+    const long long qpc = (Q + ncl - 1) / ncl;
+    const size_t smem = size_t(qpc) * v.rank * sizeof(double);
+    // measured (r01g): clusters win when a chunk is at most two load
+    // batches (C3 split tree: 12.0 -> 10.5 us per block) and lose to more,
+    // shorter chunks otherwise (C2: 38-step chunks 16.0 vs 14.6 us)
+    if (smem <= 192 * 1024 && qpc <= 2 * kTreeQB && !std::getenv("NTF_TREE_ATOMIC")) {
+      auto fn = tree_mttkrp_kernel<true>;
+      if (smem > 48 * 1024) NTF_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(unsigned(ncl), unsigned(tiles));
+      cfg.blockDim = dim3(kTreeThreads);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = s;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = unsigned(ncl);
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      NTF_CUDA(cudaLaunchKernelEx(&cfg, fn, Y, v, dF, partial, int(qpc), arrivals, out));
+      return;
+    }
+  }
   const long long qpc = (Q + chunks - 1) / chunks;
   const int nchunk = int((Q + qpc - 1) / qpc);
   const size_t smem = size_t(qpc) * v.rank * sizeof(double);
   if (smem > 200 * 1024) throw Unsupported("dimension tree: chunk too large");
   if (smem > 48 * 1024)
-    NTF_CUDA(cudaFuncSetAttribute(tree_mttkrp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-  const dim3 grid(unsigned(nchunk), unsigned(tree_tiles(v)));
-  tree_mttkrp_kernel<<<grid, kTreeThreads, smem, s>>>(Y, v, dF, partial, int(qpc), arrivals, out);
-  NTF_CUDA(cudaGetLastError());
+    NTF_CUDA(cudaFuncSetAttribute(tree_mttkrp_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(unsigned(nchunk), unsigned(tiles));
+  cfg.blockDim = dim3(kTreeThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  NTF_CUDA(cudaLaunchKernelEx(&cfg, tree_mttkrp_kernel<false>, Y, v, dF, partial, int(qpc), arrivals, out));
 }
 
 }  // namespace ntfb
