@@ -111,6 +111,10 @@ bool choose(const ModeView& v, int dtype, int sms, Choice* out) {
     const int vec = int(16 / es);
     const int bp = (cfg.B + vec - 1) / vec * vec;
     p.wld = cfg.G * bp;
+    // DMMA B fragments read 4 k rows per half-warp: a W row pitch that is a
+    // multiple of 64 B puts two (or four) of them on the same banks; pad it
+    // to 32 B off (the padding columns stay zero)
+    if (mma_try && (p.wld * es) % 64 == 0) p.wld += int(32 / es);
     if (layout == fast::kRow) {
       p.kbox = int(128 / es);
       p.nbox_r = (v.R + p.kbox - 1) / p.kbox;
