@@ -78,3 +78,29 @@ def test_dimtree_matches_direct_at_full_size(P, shape, rank):
         assert abs(a.f - b.f) <= 1e-10 * abs(a.f) + 64 * 2.0 ** -52 * prov.norm_sq()
         assert a.restarted == b.restarted
     prov.close()
+
+
+@pytest.mark.parametrize("shape,rank", [([64, 48, 40], 32), ([40, 36, 34, 32], 8)], ids=["3way", "4way-split"])
+def test_dimtree_f32_ao_trace(P, oracle, shape, rank):
+    """FP32 tensors through the dimension tree (the path BASELINE configs 4/5
+    run: FP32 partial passes with FP64 partials, FP64 tree contractions):
+    AO traces match the oracle on the float values upcast (ao.cpp:17-52) and
+    the direct GPU path to 1e-6 ||T||^2 (r01h: tree vs oracle <= 3.2e-8,
+    direct vs tree <= 1.6e-7: the FP32 factor mirrors bound it)."""
+    spec = P.SyntheticSpec(shape=shape, rank=rank, noise_sigma=0.01, seed=21)
+    t, _ = P.generate(spec, dtype=np.float32)
+    init = P.random_init(shape, rank, P.stream_seed(21, 1))
+    prov = P.GpuDenseProvider(t)
+    nsq = prov.norm_sq()
+    _, tree = P.ao_run(prov, init, P.AoConfig(max_outer_iters=20, flags=P.RUN_DIMTREE))
+    _, direct = P.ao_run(prov, init, P.AoConfig(max_outer_iters=20))
+    t64 = np.asarray(t, dtype=np.float64)
+    _, f0, recs = oracle.run("ao", t64, init.factors, max_outer_iters=20)
+    dev_o = max(abs(a.f - w["f"]) for a, w in zip(tree.records, recs)) / nsq
+    dev_d = max(abs(a.f - b.f) for a, b in zip(tree.records, direct.records)) / nsq
+    print(f"f0 dev {abs(tree.f0 - f0) / nsq:.2e}, trace dev vs oracle {dev_o:.2e}, vs direct {dev_d:.2e}")
+    assert abs(tree.f0 - f0) <= 1e-6 * nsq
+    assert len(tree.records) == len(recs) == 20
+    assert dev_o <= 1e-6 and dev_d <= 1e-6
+    assert dev_d > 0.0  # the tree path really ran (different summation order)
+    prov.close()
