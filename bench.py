@@ -7,9 +7,9 @@
 A "step" is one HER-AHALS outer iteration (N block MTTKRPs + N fused AHALS /
 extrapolation / Gram updates + the on-device restart decision) over the full
 synthetic instance. By default the block MTTKRPs use the dimension tree
-(one T x_{N-1} A_{N-1} pass shared by blocks 0..N-2, one full pass for block
-N-1; identical algorithm, summation order only); --no-dimtree runs N full
-passes. ``value`` is device-timed (CUDA events on the session
+(two full tensor passes per iteration: Y_L shared by blocks 0..h-1, Y_R by
+blocks h..N-1, h = N-1 for 3-way and N/2 for 4-way; identical algorithm,
+summation order only); --no-dimtree runs N full passes. ``value`` is device-timed (CUDA events on the session
 stream, tensor resident in HBM; the 216 MB tensor exceeds the 126 MB L2, so no
 flush is needed). ``e2e`` is the same metric through the public C-ABI driver
 ntf_her_run with host buffers: upload of the tensor and init, K iterations,

@@ -83,7 +83,7 @@ bool choose(const ModeView& v, int dtype, int sms, Choice* out) {
     MW0 = std::min(cons_cap, 8);
     n_mtiles0 = int((v.I + (long long)MW0 * RW - 1) / ((long long)MW0 * RW));
   }
-  // Tall views (the dimension tree's T x_N A_N has I = prod_{n<N-1} I_n rows)
+  // Tall views (the dimension tree's partials: Y_L has prod_{n<h} I_n rows)
   // need smaller m-tiles for a pipeline of >= 2 NP stages: fewer m-warps.
   // FP64: DMMA consumers when the blocking has them (NTF_FAST_MMA=0: DFMA)
   const char* mma_env = std::getenv("NTF_FAST_MMA");

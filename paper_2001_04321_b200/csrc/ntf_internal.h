@@ -84,8 +84,9 @@ struct ModeView {
   int fshift = 0;
 };
 
-// Dimension tree: Y = T x_{N-1} A_{N-1} (modes 0..N-2 of T, r trailing)
-// viewed around block `mode` as (L, I, R, r); see kernels_tree.cu.
+// Dimension tree: a partial Y_L (modes 0..h-1 of T, r trailing) or Y_R
+// (modes h..N-1) viewed around block `mode` as (L, I, R, r); see
+// kernels_tree.cu.
 struct TreeView {
   int order, mode, rank;  // order = number of tensor modes in the partial
   int dims[kMaxOrder];
