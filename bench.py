@@ -2,7 +2,7 @@
 """HER-AHALS outer iterations/s on BASELINE config 2 (300^3, r=20, FP64).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                  [--config c2|c3|c4|c1] [--no-dimtree]
+                  [--config c2|c3|c4|c5|c1] [--algo her|ao] [--no-dimtree]
 
 A "step" is one HER-AHALS outer iteration (N block MTTKRPs + N fused AHALS /
 extrapolation / Gram updates + the on-device restart decision) over the full
@@ -40,18 +40,42 @@ sys.path.insert(0, ROOT)
 import numpy as np  # noqa: E402
 
 CONFIGS = {
-    # name: (shape, rank, sigma, dtype, seed, BASELINE.json index)
-    "c1": ([50, 50, 50], 10, 0.01, "f64", 101, 0),
-    "c2": ([300, 300, 300], 20, 0.0, "f64", 102, 1),
-    "c3": ([100, 100, 100, 100], 16, 0.01, "f64", 103, 2),
-    "c4": ([500, 500, 500], 32, 0.01, "f32", 104, 3),
+    # name: (shape, rank, sigma, dtype, seed, BASELINE.json index, collinear)
+    "c1": ([50, 50, 50], 10, 0.01, "f64", 101, 0, False),
+    "c2": ([300, 300, 300], 20, 0.0, "f64", 102, 1, False),
+    "c3": ([100, 100, 100, 100], 16, 0.01, "f64", 103, 2, False),
+    # ill-conditioned: A_i[:, j] = 0.5 s_i + 0.5 U_i[:, j] (collinear factors,
+    # SURVEY.md §8(d) rule; bit-tested in tests/test_host_api.py)
+    "c4": ([500, 500, 500], 32, 0.01, "f32", 104, 3, True),
     # 32 GB FP32 tensor: generated with the parallel bit-exact generator (a
     # rank of a sharded run generates only its mode-1 slab)
-    "c5": ([2000, 2000, 2000], 64, 0.001, "f32", 105, 4),
+    "c5": ([2000, 2000, 2000], 64, 0.001, "f32", 105, 4, False),
 }
 LARGE = {"c5"}  # no CPU-oracle leg (the reference algorithm needs minutes per MTTKRP here)
-METRIC = "HER-AHALS outer iters/s"
 UNIT = "iters/s"
+
+
+def metric_name(algo):
+    return f"{'HER' if algo == 'her' else 'AO'}-AHALS outer iters/s"
+
+
+def workload_config(cfg_name, algo):
+    """The `config` object both arms print (identical dicts)."""
+    shape, r, sigma, dt, seed, idx, collinear = CONFIGS[cfg_name]
+    return {"workload": f"BASELINE config {idx + 1}: {'x'.join(map(str, shape))} r={r} {dt} sigma={sigma}"
+                        f"{' collinear' if collinear else ''} {'HER' if algo == 'her' else 'AO'}-AHALS",
+            "seed": seed}
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 def tree_split(order):
@@ -116,8 +140,8 @@ class ClockSampler:
 def make_instance(P, cfg_name, rank_world=(0, 1)):
     """The instance (reference generator semantics); on a sharded run only
     this rank's mode-1 slab is generated (bit-identical to that slice)."""
-    shape, rank, sigma, dt, seed, _ = CONFIGS[cfg_name]
-    spec = P.SyntheticSpec(shape=shape, rank=rank, noise_sigma=sigma, seed=seed)
+    shape, rank, sigma, dt, seed, _, collinear = CONFIGS[cfg_name]
+    spec = P.SyntheticSpec(shape=shape, rank=rank, noise_sigma=sigma, seed=seed, collinear=collinear)
     r, world = rank_world
     slab = P.slab_range(shape[0], r, world) if world > 1 else None
     t, truth = P.generate(spec, dtype=np.float32 if dt == "f32" else np.float64, slab=slab)
@@ -125,22 +149,67 @@ def make_instance(P, cfg_name, rank_world=(0, 1)):
     return t, truth, init
 
 
-def cpu_reference(cfg_name, steps, warmup, sample_only=False):
-    """The reference algorithm on the host cores (oracle restatement)."""
+def _oracle_instance(cfg_name):
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import pyoracle as O
-    shape, rank, sigma, dt, seed, _ = CONFIGS[cfg_name]
-    t, truth = O.generate(shape, rank, sigma, False, seed)
+    shape, rank, sigma, dt, seed, _, collinear = CONFIGS[cfg_name]
+    t, truth = O.generate(shape, rank, sigma, False, seed, collinear=collinear)
     if dt == "f32":
         t = t.astype(np.float32)
     init = O.random_init(shape, rank, O.stream_seed(seed, 1))
+    return O, t, init
+
+
+def cpu_reference(cfg_name, algo, steps, warmup, threads=None):
+    """The reference algorithm on the host cores (oracle restatement):
+    warmup + steps outer iterations, rate over the last `steps`."""
+    O, t, init = _oracle_instance(cfg_name)
+    if threads:
+        O.set_threads(threads)
     iters = warmup + steps
-    t0 = time.perf_counter()
-    _, f0, recs = O.run("her", t, init, max_outer_iters=iters)
-    wall = time.perf_counter() - t0
+    _, f0, recs = O.run(algo, t, init, max_outer_iters=iters)
     t_start = recs[warmup - 1]["time_s"] if warmup > 0 else 0.0
     dt_steps = recs[-1]["time_s"] - t_start
-    return steps / dt_steps, dt_steps, wall
+    return steps / dt_steps, dt_steps
+
+
+def cpu_sample(cfg_name, algo, budget_s, threads):
+    """A bounded sample: outer iterations until `budget_s` of run clock (the
+    reference's time budget, checked once per iteration), rate over the
+    iterations after the first. Returns (iters/s, iterations timed, seconds)."""
+    O, t, init = _oracle_instance(cfg_name)
+    prev = O.set_threads(threads)
+    try:
+        _, _, recs = O.run(algo, t, init, max_time_s=budget_s)
+    finally:
+        O.set_threads(prev)
+    if len(recs) >= 2:
+        n, secs = len(recs) - 1, recs[-1]["time_s"] - recs[0]["time_s"]
+    else:
+        n, secs = 1, recs[0]["time_s"]
+    return n / secs, n, secs
+
+
+def cpu_mttkrp_times(cfg_name, threads, reps=5):
+    """Per-mode CPU MTTKRP (the reference's materialised-Khatri-Rao loop,
+    kernels.cpp:161-191), best and median seconds of `reps` calls
+    (tools/kernel_bench.cpp:24-33 pattern)."""
+    O, t, init = _oracle_instance(cfg_name)
+    prev = O.set_threads(threads)
+    out = []
+    try:
+        for m in range(t.ndim):
+            ts = []
+            for _ in range(reps):
+                t0 = time.perf_counter()
+                O.mttkrp(t, init, m)
+                ts.append(time.perf_counter() - t0)
+                if ts[0] > 5.0 and len(ts) >= 3:
+                    break
+            out.append({"mode": m, "best_s": min(ts), "median_s": statistics.median(ts), "calls": len(ts)})
+    finally:
+        O.set_threads(prev)
+    return out
 
 
 def run_reference_arm(args):
@@ -148,22 +217,19 @@ def run_reference_arm(args):
     if rank != 0:
         return
     cores = os.cpu_count() or 1
-    os.environ.setdefault("OMP_NUM_THREADS", str(cores))
     if args.config in LARGE:
         print(json.dumps({"impl": "reference", "unavailable": "the reference algorithm needs the 64 GB FP64 "
                           "tensor and minutes per MTTKRP at this config; its CPU arm runs on c1-c4"}), flush=True)
         return
-    rate, secs, _ = cpu_reference(args.config, args.steps, args.warmup)
-    shape, r, sigma, dt, seed, idx = CONFIGS[args.config]
+    rate, secs = cpu_reference(args.config, args.algo, args.steps, args.warmup, threads=cores)
+    shape, r, sigma, dt, seed, idx, _ = CONFIGS[args.config]
     line = {
-        "impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": args.gpus,
+        "impl": "reference", "metric": metric_name(args.algo), "value": rate, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": dt,
         "data": "synthetic (reference generator semantics, seeded)",
-        "config": {"workload": f"BASELINE config {idx + 1}: {'x'.join(map(str, shape))} r={r} sigma={sigma} "
-                               f"HER-AHALS", "seed": seed},
-        "cpu_baseline": {"value": rate, "unit": UNIT, "cores": int(os.environ["OMP_NUM_THREADS"]),
-                         "kind": "port",
+        "config": workload_config(args.config, args.algo),
+        "cpu_baseline": {"value": rate, "unit": UNIT, "cores": cores, "kind": "port", "cpu": cpu_model(),
                          "sample": f"{args.warmup}+{args.steps} outer iterations of the full instance; the "
                                    "reference (needs Eigen3) cannot be built, so the oracle restatement of its "
                                    "algorithm runs (OpenMP over output rows, materialised Khatri-Rao)"},
@@ -190,7 +256,7 @@ def run_ours(args):
     else:
         ctx = P.Context(local)
 
-    shape, r, sigma, dt, seed, idx = CONFIGS[args.config]
+    shape, r, sigma, dt, seed, idx, _ = CONFIGS[args.config]
     t_gen, truth, init = make_instance(P, args.config, (rank, world))
     itemsize = 4 if dt == "f32" else 8
     # the caller's tensor lives in pinned host memory (the e2e contract), so
@@ -203,13 +269,11 @@ def run_ours(args):
         del t_gen
     except Exception as exc:  # pinning refused: pageable memory, said in the line
         t_local, pinned = t_gen, f"pageable ({type(exc).__name__})"
-    flags = 0
-    if args.dimtree:
-        flags |= 1
+    flags = 0 if args.dimtree else P.RUN_DIRECT  # the dimension tree is the library default
     cfg = P.AoConfig(max_outer_iters=args.warmup + args.steps + 10**6, flags=flags)
 
     prov = P.GpuDenseProvider(t_local, ctx, full_shape=shape)
-    sess = P.Session(prov, init, cfg, P.HerParams(), algo="her")
+    sess = P.Session(prov, init, cfg, P.HerParams(), algo=args.algo)
     stream = torch.cuda.ExternalStream(sess.stream_ptr)
 
     def barrier():
@@ -281,8 +345,11 @@ def run_ours(args):
         barrier()
         t0 = time.perf_counter()
         prov2 = P.GpuDenseProvider(t_local, ctx, full_shape=shape)
-        model, tr2 = P.her_run(prov2, init, P.AoConfig(max_outer_iters=args.steps, flags=flags), P.HerParams(),
-                               ctx=ctx)
+        ecfg = P.AoConfig(max_outer_iters=args.steps, flags=flags)
+        if args.algo == "her":
+            model, tr2 = P.her_run(prov2, init, ecfg, P.HerParams(), ctx=ctx)
+        else:
+            model, tr2 = P.ao_run(prov2, init, ecfg, ctx=ctx)
         e2e_s = time.perf_counter() - t0
         prov2.close()
         if world > 1:
@@ -298,19 +365,24 @@ def run_ours(args):
         fp32_peak = 71.7
         cpu = None
         if world == 1 and not args.no_cpu_baseline and args.config not in LARGE:
-            os.environ.setdefault("OMP_NUM_THREADS", str(os.cpu_count() or 1))
-            rate, secs, _ = cpu_reference(args.config, steps=args.cpu_steps, warmup=1)
-            cpu = {"value": rate, "unit": UNIT, "cores": int(os.environ["OMP_NUM_THREADS"]), "kind": "port",
-                   "sample": f"1+{args.cpu_steps} HER-AHALS outer iterations of the full instance (oracle "
-                             "restatement of the reference algorithm, OpenMP)"}
+            cores = os.cpu_count() or 1
+            rate, n_it, secs = cpu_sample(args.config, args.algo, args.cpu_budget, cores)
+            cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "port", "cpu": cpu_model(),
+                   "sample": f"{n_it} outer iterations ({secs:.1f} s) after one warm-up iteration, run under the "
+                             f"reference's time budget of {args.cpu_budget:g} s on the full instance (oracle "
+                             "restatement of the reference algorithm, OpenMP over all cores)"}
+            if args.config != "c4":  # one reference iteration at c4 is minutes on one core
+                r1, n1, s1 = cpu_sample(args.config, args.algo, args.cpu_budget, 1)
+                cpu["single_thread"] = {"value": r1, "unit": UNIT, "cores": 1, "iterations": n1, "seconds": s1}
+            cpu["mttkrp_per_mode"] = cpu_mttkrp_times(args.config, cores)
         line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "metric": metric_name(args.algo), "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": dt,
             "data": "synthetic (reference generator semantics, seeded; random U[0,1) init)",
-            "config": {"workload": f"BASELINE config {idx + 1}: {'x'.join(map(str, shape))} r={r} sigma={sigma} "
-                                   f"HER-AHALS", "seed": seed, "l2": "tensor larger than L2 (no flush)",
-                       "parallelism": f"mode-1 slabs x{world}", "dimtree": bool(args.dimtree)},
+            "config": workload_config(args.config, args.algo),
+            "run": {"l2": "tensor larger than L2 (no flush)", "parallelism": f"mode-1 slabs x{world}",
+                    "dimtree": bool(args.dimtree), "graph": True},
             "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm_peak, "unit": "GB/s",
                          "frac": achieved_gbs / hbm_peak, "traffic": traffic, "peak_kind": peak_kind,
                          "traffic_source": "profiles/traffic.json (ncu dram__bytes_read+write per launch)",
@@ -346,7 +418,9 @@ def main():
     # algorithm, 2 full tensor passes per outer iteration instead of N
     ap.add_argument("--dimtree", dest="dimtree", action="store_true", default=True)
     ap.add_argument("--no-dimtree", dest="dimtree", action="store_false")
-    ap.add_argument("--cpu-steps", type=int, default=3)
+    ap.add_argument("--algo", default="her", choices=["her", "ao"])
+    ap.add_argument("--cpu-budget", type=float, default=12.0,
+                    help="seconds of reference run clock for each CPU baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:

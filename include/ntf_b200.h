@@ -60,10 +60,16 @@ typedef struct {
 } ntf_inner_stop;
 
 /* Performance options of the GPU drivers (no reference counterpart). */
-#define NTF_RUN_DIMTREE 1u  /* dimension tree: two partial contractions per
-                               sweep (Y_L, Y_R) instead of N full passes    */
+/* The drivers use the dimension tree by default: two full tensor passes per
+ * outer iteration (Y_L, Y_R) plus small contractions instead of N full
+ * passes -- the same algorithm, only the summation order of the MTTKRPs
+ * differs. NTF_RUN_DIMTREE is accepted for compatibility (it is the default);
+ * NTF_RUN_DIRECT selects the reference's loop shape (one full MTTKRP pass per
+ * block, kernels.cpp:161-191). */
+#define NTF_RUN_DIMTREE 1u  /* default; kept for compatibility                */
 #define NTF_RUN_NO_GRAPH 2u /* launch kernels directly instead of a CUDA graph */
 #define NTF_RUN_GENERIC 4u  /* force the generic MTTKRP kernel (testing)     */
+#define NTF_RUN_DIRECT 8u   /* N full MTTKRP passes per iteration (no tree)   */
 
 /* AoConfig (include/ntf/ao.hpp:15-24). `ground_truth` is a concatenated
  * factor model (same shape and rank as the init) and is required when
@@ -167,7 +173,10 @@ int ntf_ctx_create(int device, ntf_ctx** out);
 /* NCCL unique id for ntf_ctx_create_dist (128 bytes, rank 0 creates it). */
 int ntf_nccl_unique_id(unsigned char out[128]);
 /* One rank of a world of `world` GPUs on one node; the mode-1 slab of the
- * tensor lives on this rank. */
+ * tensor lives on this rank. world = 1 creates a one-rank
+ * communicator: the drivers then run the sharded code path (allgather +
+ * row compaction for mode 1, allreduce for the other modes, collective time
+ * budget) on one GPU. */
 int ntf_ctx_create_dist(int device, int rank, int world, const unsigned char id[128], ntf_ctx** out);
 int ntf_ctx_info(const ntf_ctx* ctx, int* device, int* rank, int* world);
 int ntf_ctx_destroy(ntf_ctx* ctx);
@@ -181,9 +190,26 @@ int ntf_slab_range(int64_t dim0, int rank, int world, int64_t* begin, int64_t* e
  * once in FP64 (DenseProvider ctor, provider.cpp:7; tensor.cpp:43-47). */
 int ntf_tensor_upload(ntf_ctx* ctx, const void* host, int dtype, int order, const int64_t* shape,
                       ntf_tensor** out);
-/* Same, from a device buffer of this context's GPU (copied). */
+/* Same, from a device buffer of this context's GPU (copied). Ordering: the
+ * copy runs on the context's own stream, so the caller's producer work must
+ * be complete -- this entry point synchronises the device before copying.
+ * ntf_tensor_upload_device_async instead orders the copy after all work
+ * enqueued so far on `caller_stream` (a cudaStream_t as void*, NULL = the
+ * legacy default stream) without blocking the host. */
 int ntf_tensor_upload_device(ntf_ctx* ctx, const void* dev, int dtype, int order,
                              const int64_t* shape, ntf_tensor** out);
+int ntf_tensor_upload_device_async(ntf_ctx* ctx, const void* dev, int dtype, int order,
+                                   const int64_t* shape, void* caller_stream, ntf_tensor** out);
+/* A caller-chosen mode-1 row slab [row_begin, row_end) of a tensor of FULL
+ * shape `shape` on a 1-GPU context (`host` holds only those rows). This is
+ * the per-rank piece of the sharded path made callable on
+ * one GPU: ntf_mttkrp / ntf_mttkrp_all then return this slab's
+ * contribution -- for mode 1 the slab's rows (the other rows zero), for the
+ * other modes the slab's partial I_n x r sum -- so the MTTKRP of the whole
+ * tensor is the sum over a row partition. ||T||^2 is the slab's. Driver
+ * runs (her/ao/session) reject such a tensor. */
+int ntf_tensor_upload_rows(ntf_ctx* ctx, const void* host, int dtype, int order, const int64_t* shape,
+                           int64_t row_begin, int64_t row_end, ntf_tensor** out);
 /* ObjectiveProvider::shape / norm_sq (provider.hpp:16-17). */
 int ntf_tensor_shape(const ntf_tensor* t, int* order, int64_t* shape);
 int ntf_tensor_norm_sq(const ntf_tensor* t, double* out);
@@ -194,9 +220,19 @@ int ntf_tensor_destroy(ntf_tensor* t);
  * pinned staging buffers, rounded to FP32 when dtype is NTF_DTYPE_F32. */
 int ntf_tensor_upload_ntft(ntf_ctx* ctx, const char* path, int dtype, ntf_tensor** out);
 /* ObjectiveProvider::mttkrp (provider.hpp:18; kernels.cpp:161-191): out is
- * the I_mode x rank MTTKRP (row-major, FP64), identical on every rank. */
+ * the I_mode x rank MTTKRP (row-major, FP64), identical on every rank. The
+ * tensor keeps the kernel plan and device workspaces of its last (rank)
+ * between calls, so a provider loop pays the factor upload and one kernel
+ * per call. */
 int ntf_mttkrp(ntf_ctx* ctx, const ntf_tensor* t, const double* factors, int rank, int mode,
                double* out);
+/* Every mode's MTTKRP at one fixed model, in sweep order 0..N-1, written
+ * concatenated (mode n at offset sum_{m<n} I_m * rank). flags: 0 = the
+ * dimension tree the drivers use (two full passes + contractions),
+ * NTF_RUN_DIRECT = N full passes, NTF_RUN_GENERIC = the generic kernel.
+ * Repeated calls on one tensor reuse its plan and device workspaces. */
+int ntf_mttkrp_all(ntf_ctx* ctx, const ntf_tensor* t, const double* factors, int rank, unsigned flags,
+                   double* out);
 /* objective(t, m, cache, pivot) (kernels.cpp:305-311): one MTTKRP at `pivot`
  * (-1 = last mode) plus the cheap objective. */
 int ntf_objective(ntf_ctx* ctx, const ntf_tensor* t, const double* factors, int rank, int pivot,

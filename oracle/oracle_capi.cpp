@@ -1,6 +1,8 @@
 // TEST INFRASTRUCTURE ONLY — extern "C" surface of the CPU oracle, loaded by
 // tests/ (ctypes) and by bench.py's cpu_baseline / --impl reference legs.
 // Factor matrices cross this boundary row-major, modes concatenated.
+#include <omp.h>
+
 #include <cstring>
 #include <exception>
 #include <stdexcept>
@@ -269,3 +271,11 @@ int ora_run(int algo, const void* tensor, int dtype, const int* shape, int order
 }
 
 }  // extern "C"
+
+// OpenMP thread count of the oracle's parallel loops (bench.py's 1-thread and
+// all-core CPU baselines); returns the previous maximum.
+extern "C" int ora_set_threads(int n) {
+  const int prev = omp_get_max_threads();
+  if (n > 0) omp_set_num_threads(n);
+  return prev;
+}

@@ -57,6 +57,8 @@ def lib():
         L.ora_update_betas.argtypes = [_dptr, C.c_int, C.c_double, C.c_double, C.c_double, C.c_double]
         L.ora_validate_her_params.argtypes = [C.c_double] * 4
         L.ora_extrapolate.argtypes = [_dptr, _dptr, C.c_int, C.c_int, C.c_double, _dptr]
+        L.ora_set_threads.restype = C.c_int
+        L.ora_set_threads.argtypes = [C.c_int]
         _LIB = L
     return _LIB
 
@@ -88,6 +90,11 @@ def _split(flat, shape, rank):
         out.append(flat[off:off + d * rank].reshape(d, rank).copy())
         off += d * rank
     return out
+
+
+def set_threads(n):
+    """OpenMP threads of the oracle's parallel loops; returns the previous maximum."""
+    return int(lib().ora_set_threads(int(n)))
 
 
 def stream_seed(base, stream):

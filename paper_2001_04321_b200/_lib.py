@@ -27,6 +27,7 @@ NTF_DTYPE_F32 = 1
 NTF_RUN_DIMTREE = 1
 NTF_RUN_NO_GRAPH = 2
 NTF_RUN_GENERIC = 4
+NTF_RUN_DIRECT = 8
 
 dptr = C.POINTER(C.c_double)
 iptr = C.POINTER(C.c_int)
@@ -89,10 +90,15 @@ SIGNATURES = {
     "ntf_tensor_upload": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, i64ptr, C.POINTER(C.c_void_p)]),
     "ntf_tensor_upload_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, i64ptr,
                                            C.POINTER(C.c_void_p)]),
+    "ntf_tensor_upload_device_async": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, i64ptr, C.c_void_p,
+                                                 C.POINTER(C.c_void_p)]),
+    "ntf_tensor_upload_rows": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, i64ptr, C.c_int64, C.c_int64,
+                                         C.POINTER(C.c_void_p)]),
     "ntf_tensor_shape": (C.c_int, [C.c_void_p, iptr, i64ptr]),
     "ntf_tensor_norm_sq": (C.c_int, [C.c_void_p, dptr]),
     "ntf_tensor_destroy": (C.c_int, [C.c_void_p]),
     "ntf_mttkrp": (C.c_int, [C.c_void_p, C.c_void_p, dptr, C.c_int, C.c_int, dptr]),
+    "ntf_mttkrp_all": (C.c_int, [C.c_void_p, C.c_void_p, dptr, C.c_int, C.c_uint, dptr]),
     "ntf_mttkrp_plan": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_char_p, C.c_size_t]),
     "ntf_objective": (C.c_int, [C.c_void_p, C.c_void_p, dptr, C.c_int, C.c_int, dptr]),
     "ntf_solve_nnls": (C.c_int, [C.c_void_p, C.c_int, dptr, dptr, dptr, C.c_int, C.c_int,

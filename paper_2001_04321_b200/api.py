@@ -89,10 +89,13 @@ def nnls_solver_from_name(name: str) -> NnlsSolver:
     return table[name]
 
 
-# NTF_RUN_* performance options of AoConfig.flags (include/ntf_b200.h)
-RUN_DIMTREE = 1   # dimension-tree MTTKRP reuse: 2 tensor passes per outer iteration
+# NTF_RUN_* performance options of AoConfig.flags (include/ntf_b200.h). The
+# dimension tree (2 full tensor passes per outer iteration instead of N; the
+# same algorithm up to MTTKRP summation order) is the default.
+RUN_DIMTREE = 1   # accepted for compatibility: the tree is the default
 RUN_NO_GRAPH = 2  # enqueue every iteration directly (no CUDA graph)
 RUN_GENERIC = 4   # generic MTTKRP kernel only (diagnostics)
+RUN_DIRECT = 8    # N full MTTKRP passes per iteration (the reference's loop shape)
 
 
 @dataclasses.dataclass
@@ -372,8 +375,10 @@ class Context:
     """One GPU (or one rank of an NCCL world) — owns streams and the NCCL comm."""
 
     def __init__(self, device=0, rank=0, world=1, nccl_id: Optional[bytes] = None):
+        """``nccl_id`` with world 1 makes a one-rank NCCL communicator (the
+        sharded code path on one GPU)."""
         h = C.c_void_p()
-        if world == 1:
+        if world == 1 and nccl_id is None:
             _check(L.lib().ntf_ctx_create(device, C.byref(h)))
         else:
             if nccl_id is None or len(nccl_id) != 128:
@@ -440,10 +445,17 @@ class GpuDenseProvider(ObjectiveProvider):
 
     ``tensor``: numpy float64/float32 array holding the full tensor (or, on a
     multi-rank context, this rank's mode-1 slab with ``full_shape`` given), or
-    a CUDA torch tensor on the context's device.
+    a CUDA torch tensor on the context's device (the copy is ordered after
+    the work already enqueued on torch's current stream).
+
+    ``rows=(begin, end)`` with ``full_shape``: ``tensor`` holds only those
+    mode-1 rows of the full tensor, on a 1-GPU context (ntf_tensor_upload_rows:
+    the per-rank piece of the sharded path; ``mttkrp`` then returns the
+    slab's contribution and the whole tensor's MTTKRP is the sum over a row
+    partition).
     """
 
-    def __init__(self, tensor, ctx: Optional[Context] = None, full_shape=None):
+    def __init__(self, tensor, ctx: Optional[Context] = None, full_shape=None, rows=None):
         self.ctx = ctx or default_context()
         h = C.c_void_p()
         if hasattr(tensor, "is_cuda") and tensor.is_cuda:
@@ -454,8 +466,23 @@ class GpuDenseProvider(ObjectiveProvider):
             shape = list(full_shape or tensor.shape)
             code = L.NTF_DTYPE_F32 if tensor.dtype == torch.float32 else L.NTF_DTYPE_F64
             arr = (C.c_int64 * len(shape))(*shape)
-            _check(L.lib().ntf_tensor_upload_device(self.ctx.handle, C.c_void_p(tensor.data_ptr()), code,
-                                                    len(shape), arr, C.byref(h)))
+            stream = torch.cuda.current_stream(tensor.device).cuda_stream
+            _check(L.lib().ntf_tensor_upload_device_async(self.ctx.handle, C.c_void_p(tensor.data_ptr()), code,
+                                                          len(shape), arr, C.c_void_p(stream), C.byref(h)))
+        elif rows is not None:
+            t = np.ascontiguousarray(np.asarray(tensor))
+            if t.dtype not in (np.float32, np.float64):
+                t = t.astype(np.float64)
+            if full_shape is None:
+                raise InvalidArgument("rows= needs full_shape")
+            shape = list(full_shape)
+            code = L.NTF_DTYPE_F32 if t.dtype == np.float32 else L.NTF_DTYPE_F64
+            arr = (C.c_int64 * len(shape))(*shape)
+            b, e = int(rows[0]), int(rows[1])
+            if t.size != (e - b) * int(np.prod(shape[1:])):
+                raise InvalidArgument("rows= slab size does not match the tensor data")
+            _check(L.lib().ntf_tensor_upload_rows(self.ctx.handle, t.ctypes.data_as(C.c_void_p), code, len(shape),
+                                                  arr, b, e, C.byref(h)))
         else:
             t = np.asarray(tensor)
             if t.dtype not in (np.float32, np.float64):
@@ -508,6 +535,19 @@ class GpuDenseProvider(ObjectiveProvider):
         out = np.empty((self._shape[mode], m.rank()))
         _check(L.lib().ntf_mttkrp(self.ctx.handle, self.handle, _dp(flat), m.rank(), mode, _dp(out)))
         return out
+
+    def mttkrp_all(self, model, flags=0):
+        """Every mode's MTTKRP at one model, in sweep order (ntf_mttkrp_all):
+        flags 0 = the dimension tree the drivers use, RUN_DIRECT = N full
+        passes, RUN_GENERIC = the generic kernel. Returns a list of I_n x r."""
+        m, flat = self._model_flat(model)
+        out = np.empty(sum(self._shape) * m.rank())
+        _check(L.lib().ntf_mttkrp_all(self.ctx.handle, self.handle, _dp(flat), m.rank(), int(flags), _dp(out)))
+        res, off = [], 0
+        for d in self._shape:
+            res.append(out[off:off + d * m.rank()].reshape(d, m.rank()).copy())
+            off += d * m.rank()
+        return res
 
     def mttkrp_plan(self, rank, mode):
         """Which kernel ntf_mttkrp runs for (rank, mode): 'generic' or the fast blocking."""

@@ -3,7 +3,9 @@
 // buffer read by ntf_last_error().
 #include <nccl.h>
 
+#include <algorithm>
 #include <chrono>
+#include <memory>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -96,8 +98,11 @@ void check_run_inputs(const ntf_tensor* t, const double* init, int rank, const n
 // The tensor handle of this rank's mode-1 slab; `fill` copies the slab's
 // n_local values into t->data on ctx->stream. ||T||^2 follows (FP64,
 // all-reduced over the ranks).
+// rows = {begin, end} picks a caller-chosen mode-1 slab on a 1-GPU context
+// (ntf_tensor_upload_rows); {-1, -1} = this rank's slab_range.
 template <typename Fill>
-ntf_tensor* make_tensor_with(ntf_ctx* ctx, int dtype, int order, const int64_t* shape, Fill&& fill) {
+ntf_tensor* make_tensor_with(ntf_ctx* ctx, int dtype, int order, const int64_t* shape, Fill&& fill,
+                             long long rows_b = -1, long long rows_e = -1) {
   need(ctx, "ctx");
   need(shape, "shape");
   if (dtype != NTF_DTYPE_F64 && dtype != NTF_DTYPE_F32) throw InvalidArgument("unknown dtype");
@@ -112,7 +117,15 @@ ntf_tensor* make_tensor_with(ntf_ctx* ctx, int dtype, int order, const int64_t* 
       t->shape[i] = shape[i];
     }
     long long b = 0, e = shape[0];
-    slab_range(shape[0], ctx->comm.rank, ctx->comm.world, &b, &e);
+    if (rows_b >= 0) {
+      if (ctx->comm.active()) throw InvalidArgument("explicit row slabs need a 1-GPU context without NCCL");
+      if (rows_e <= rows_b || rows_e > shape[0]) throw InvalidArgument("row slab outside the first mode");
+      b = rows_b;
+      e = rows_e;
+      t->rows_only = (b != 0 || e != shape[0]);
+    } else {
+      slab_range(shape[0], ctx->comm.rank, ctx->comm.world, &b, &e);
+    }
     t->row0 = b;
     t->rows = e - b;
     if (t->rows < 1) throw InvalidArgument("every rank needs at least one mode-1 row");
@@ -136,39 +149,59 @@ ntf_tensor* make_tensor_with(ntf_ctx* ctx, int dtype, int order, const int64_t* 
 }
 
 ntf_tensor* make_tensor(ntf_ctx* ctx, const void* src, bool src_on_device, int dtype, int order,
-                        const int64_t* shape) {
+                        const int64_t* shape, long long rows_b = -1, long long rows_e = -1) {
   need(src, "tensor data");
-  return make_tensor_with(ctx, dtype, order, shape, [&](ntf_tensor* t) {
-    const size_t es = dtype == NTF_DTYPE_F32 ? 4 : 8;
-    NTF_CUDA(cudaMemcpyAsync(t->data.p, src, size_t(t->n_local) * es,
-                             src_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, ctx->stream));
-  });
+  return make_tensor_with(
+      ctx, dtype, order, shape,
+      [&](ntf_tensor* t) {
+        const size_t es = dtype == NTF_DTYPE_F32 ? 4 : 8;
+        NTF_CUDA(cudaMemcpyAsync(t->data.p, src, size_t(t->n_local) * es,
+                                 src_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, ctx->stream));
+      },
+      rows_b, rows_e);
 }
 
-// A DevFactors over caller factors (sel = 0 for every mode), for the
-// per-call provider entry points.
-struct TempFactors {
-  DevBuf fac, grams, dF;
-  DevFactors h{};
-  TempFactors(const ntf_tensor* t, const double* factors, int rank, cudaStream_t s) {
-    const long long n = model_len(t, rank);
-    fac = DevBuf(size_t(n) * sizeof(double));
-    grams = DevBuf(size_t(t->order) * rank * rank * sizeof(double));
-    dF = DevBuf(sizeof(DevFactors));
-    std::memset(&h, 0, sizeof h);
-    h.order = t->order;
-    h.rank = rank;
+// The per-call provider workspace of tensor t for (rank, flags): engine,
+// factor buffers (one buffer per mode, both roles alias it) and Grams /
+// FP32 mirrors of `factors`, which are uploaded on ctx->stream.
+CallCache& call_setup(ntf_ctx* ctx, const ntf_tensor* t, const double* factors, int rank, unsigned flags) {
+  need(factors, "factors");
+  if (rank < 1) throw InvalidArgument("rank must be >= 1");
+  NTF_CUDA(cudaSetDevice(ctx->device));
+  auto& c = t->cache;
+  if (!c || c->rank != rank || c->flags != flags) {
+    if (c) NTF_CUDA(cudaStreamSynchronize(ctx->stream));
+    c.reset();
+    auto n = std::make_unique<CallCache>();
+    n->rank = rank;
+    n->flags = flags;
+    n->eng = std::make_unique<MttkrpEngine>(ctx, t, rank, flags);
+    const long long len = model_len(t, rank);
+    n->fac = DevBuf(size_t(len) * sizeof(double));
+    if (t->dtype == NTF_DTYPE_F32) n->fac32 = DevBuf(size_t(len) * sizeof(float));
+    n->grams = DevBuf(size_t(t->order) * rank * rank * sizeof(double));
+    n->dF = DevBuf(sizeof(DevFactors));
+    long long maxrows = 0;
+    for (int i = 0; i < t->order; ++i) maxrows = std::max(maxrows, t->shape[i]);
+    n->C = DevBuf(size_t(maxrows) * rank * sizeof(double));
+    std::memset(&n->h, 0, sizeof n->h);
+    n->h.order = t->order;
+    n->h.rank = rank;
     long long off = 0;
     for (int i = 0; i < t->order; ++i) {
-      h.x[i][0] = h.x[i][1] = fac.as<double>() + off;
-      h.gram[i][0] = h.gram[i][1] = grams.as<double>() + size_t(i) * rank * rank;
-      h.rows[i] = int(t->shape[i]);
+      n->h.x[i][0] = n->h.x[i][1] = n->fac.as<double>() + off;
+      if (n->fac32.p) n->h.x32[i][0] = n->h.x32[i][1] = n->fac32.as<float>() + off;
+      n->h.gram[i][0] = n->h.gram[i][1] = n->grams.as<double>() + size_t(i) * rank * rank;
+      n->h.rows[i] = int(t->shape[i]);
       off += t->shape[i] * rank;
     }
-    NTF_CUDA(cudaMemcpyAsync(fac.p, factors, size_t(n) * sizeof(double), cudaMemcpyHostToDevice, s));
-    NTF_CUDA(cudaMemcpyAsync(dF.p, &h, sizeof h, cudaMemcpyHostToDevice, s));
+    NTF_CUDA(cudaMemcpyAsync(n->dF.p, &n->h, sizeof n->h, cudaMemcpyHostToDevice, ctx->stream));
+    c = std::move(n);
   }
-};
+  NTF_CUDA(cudaMemcpyAsync(c->fac.p, factors, c->fac.bytes, cudaMemcpyHostToDevice, ctx->stream));
+  launch_init_factors(c->dF.as<DevFactors>(), c->h, ctx->stream);
+  return *c;
+}
 
 void run_driver(int algo, ntf_ctx* ctx, const ntf_tensor* t, const double* init, int rank,
                 const ntf_ao_config* cfg, const ntf_her_params* params, ntf_her_observer observer, void* user,
@@ -204,7 +237,6 @@ void run_driver(int algo, ntf_ctx* ctx, const ntf_tensor* t, const double* init,
               ms(t2, now()));
   } else {
     std::vector<double> acc(static_cast<size_t>(len));
-    std::vector<ntf_trace_record> last(1);
     while (true) {
       s.step(1);
       s.sync();
@@ -214,14 +246,13 @@ void run_driver(int algo, ntf_ctx* ctx, const ntf_tensor* t, const double* init,
       if (cfg->record_factor_error)
         e_values.push_back(factor_error(acc.data(), cfg->ground_truth, shape.data(), t->order, rank));
       if (observer) {
-        std::vector<ntf_trace_record> all(static_cast<size_t>(k));
-        int n = 0;
-        s.trace(nullptr, all.data(), k, &n);
+        ntf_trace_record last{};
+        s.last_record(&last);
         ntf_her_iteration_info info{};
         info.iter = k;
-        info.f_hat = all[size_t(k - 1)].f;
-        info.restarted = all[size_t(k - 1)].restarted;
-        info.beta_used = all[size_t(k - 1)].beta;
+        info.f_hat = last.f;
+        info.restarted = last.restarted;
+        info.beta_used = last.beta;
         info.factors = acc.data();
         info.hat_factors = acc.data();  // equal after every decision (her.cpp:76-83)
         observer(&info, user);
@@ -385,7 +416,7 @@ int ntf_ctx_create_dist(int device, int rank, int world, const unsigned char id[
     try {
       c->comm.rank = rank;
       c->comm.world = world;
-      if (world > 1) {
+      {  // world 1 too: a 1-rank communicator runs the collective path on one GPU
         ncclUniqueId uid;
         std::memcpy(&uid, id, 128);
         ncclComm_t comm;
@@ -476,7 +507,35 @@ int ntf_tensor_upload_device(ntf_ctx* ctx, const void* dev, int dtype, int order
                              ntf_tensor** out) {
   return guarded([&] {
     need(out, "out");
+    need(ctx, "ctx");
+    NTF_CUDA(cudaSetDevice(ctx->device));
+    NTF_CUDA(cudaDeviceSynchronize());  // the producer of `dev` ran on some other stream
     *out = make_tensor(ctx, dev, true, dtype, order, shape);
+  });
+}
+
+int ntf_tensor_upload_device_async(ntf_ctx* ctx, const void* dev, int dtype, int order, const int64_t* shape,
+                                   void* caller_stream, ntf_tensor** out) {
+  return guarded([&] {
+    need(out, "out");
+    need(ctx, "ctx");
+    NTF_CUDA(cudaSetDevice(ctx->device));
+    cudaEvent_t ev;
+    NTF_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    const cudaError_t e1 = cudaEventRecord(ev, static_cast<cudaStream_t>(caller_stream));
+    const cudaError_t e2 = e1 == cudaSuccess ? cudaStreamWaitEvent(ctx->stream, ev, 0) : e1;
+    cudaEventDestroy(ev);
+    NTF_CUDA(e2);
+    *out = make_tensor(ctx, dev, true, dtype, order, shape);
+  });
+}
+
+int ntf_tensor_upload_rows(ntf_ctx* ctx, const void* host, int dtype, int order, const int64_t* shape,
+                           int64_t row_begin, int64_t row_end, ntf_tensor** out) {
+  return guarded([&] {
+    need(out, "out");
+    if (row_begin < 0) throw InvalidArgument("row slab outside the first mode");
+    *out = make_tensor(ctx, host, false, dtype, order, shape, (long long)row_begin, (long long)row_end);
   });
 }
 
@@ -508,32 +567,32 @@ int ntf_mttkrp(ntf_ctx* ctx, const ntf_tensor* t, const double* factors, int ran
   return guarded([&] {
     need(ctx, "ctx");
     need(t, "tensor");
-    need(factors, "factors");
     need(out, "out");
-    if (rank < 1) throw InvalidArgument("rank must be >= 1");
     if (mode < 0 || mode >= t->order) throw InvalidArgument("mode out of range");
-    NTF_CUDA(cudaSetDevice(ctx->device));
-    TempFactors tf(t, factors, rank, ctx->stream);
-    if (t->dtype == NTF_DTYPE_F32) {  // FP32 mirrors for the FP32 kernels
-      DevBuf f32(size_t(model_len(t, rank)) * sizeof(float));
-      long long off = 0;
-      for (int i = 0; i < t->order; ++i) {
-        tf.h.x32[i][0] = tf.h.x32[i][1] = f32.as<float>() + off;
-        off += t->shape[i] * rank;
-      }
-      NTF_CUDA(cudaMemcpyAsync(tf.dF.p, &tf.h, sizeof tf.h, cudaMemcpyHostToDevice, ctx->stream));
-      launch_init_factors(tf.dF.as<DevFactors>(), tf.h, ctx->stream);
-      MttkrpEngine eng(ctx, t, rank, 0);
-      DevBuf C(size_t(t->shape[mode]) * rank * sizeof(double));
-      eng.run(mode, tf.dF.as<DevFactors>(), C.as<double>(), ctx->stream);
-      NTF_CUDA(cudaMemcpyAsync(out, C.p, C.bytes, cudaMemcpyDeviceToHost, ctx->stream));
-      NTF_CUDA(cudaStreamSynchronize(ctx->stream));
-      return;
+    CallCache& c = call_setup(ctx, t, factors, rank, NTF_RUN_DIRECT);
+    c.eng->run(mode, c.dF.as<DevFactors>(), c.C.as<double>(), ctx->stream);
+    NTF_CUDA(cudaMemcpyAsync(out, c.C.p, size_t(t->shape[mode]) * rank * sizeof(double), cudaMemcpyDeviceToHost,
+                             ctx->stream));
+    NTF_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int ntf_mttkrp_all(ntf_ctx* ctx, const ntf_tensor* t, const double* factors, int rank, unsigned flags,
+                   double* out) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(t, "tensor");
+    need(out, "out");
+    if (flags & ~(NTF_RUN_DIMTREE | NTF_RUN_DIRECT | NTF_RUN_GENERIC | NTF_RUN_NO_GRAPH))
+      throw InvalidArgument("unknown NTF_RUN_* flags");
+    CallCache& c = call_setup(ctx, t, factors, rank, flags & (NTF_RUN_DIRECT | NTF_RUN_GENERIC));
+    long long off = 0;
+    for (int m = 0; m < t->order; ++m) {  // sweep order: the tree forms Y_L at block 0, Y_R at block h
+      c.eng->run(m, c.dF.as<DevFactors>(), c.C.as<double>(), ctx->stream);
+      const size_t n = size_t(t->shape[m]) * rank;
+      NTF_CUDA(cudaMemcpyAsync(out + off, c.C.p, n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+      off += (long long)n;
     }
-    MttkrpEngine eng(ctx, t, rank, 0);
-    DevBuf C(size_t(t->shape[mode]) * rank * sizeof(double));
-    eng.run(mode, tf.dF.as<DevFactors>(), C.as<double>(), ctx->stream);
-    NTF_CUDA(cudaMemcpyAsync(out, C.p, C.bytes, cudaMemcpyDeviceToHost, ctx->stream));
     NTF_CUDA(cudaStreamSynchronize(ctx->stream));
   });
 }
@@ -543,8 +602,9 @@ int ntf_mttkrp_plan(ntf_ctx* ctx, const ntf_tensor* t, int rank, int mode, char*
     need(ctx, "ctx");
     need(t, "tensor");
     need(buf, "buf");
+    if (rank < 1) throw InvalidArgument("rank must be >= 1");
     if (mode < 0 || mode >= t->order) throw InvalidArgument("mode out of range");
-    MttkrpEngine eng(ctx, t, rank, 0);
+    MttkrpEngine eng(ctx, t, rank, NTF_RUN_DIRECT);
     const std::string s = eng.describe(mode);
     if (n) {
       std::strncpy(buf, s.c_str(), n - 1);
@@ -557,29 +617,14 @@ int ntf_objective(ntf_ctx* ctx, const ntf_tensor* t, const double* factors, int 
   return guarded([&] {
     need(ctx, "ctx");
     need(t, "tensor");
-    need(factors, "factors");
     need(out, "out");
-    if (rank < 1) throw InvalidArgument("rank must be >= 1");
     const int p = pivot < 0 ? t->order - 1 : pivot;
     if (p >= t->order) throw InvalidArgument("mode out of range");
-    NTF_CUDA(cudaSetDevice(ctx->device));
-    TempFactors tf(t, factors, rank, ctx->stream);
-    DevBuf f32;
-    if (t->dtype == NTF_DTYPE_F32) {
-      f32 = DevBuf(size_t(model_len(t, rank)) * sizeof(float));
-      long long off = 0;
-      for (int i = 0; i < t->order; ++i) {
-        tf.h.x32[i][0] = tf.h.x32[i][1] = f32.as<float>() + off;
-        off += t->shape[i] * rank;
-      }
-      NTF_CUDA(cudaMemcpyAsync(tf.dF.p, &tf.h, sizeof tf.h, cudaMemcpyHostToDevice, ctx->stream));
-    }
-    launch_init_factors(tf.dF.as<DevFactors>(), tf.h, ctx->stream);
-    MttkrpEngine eng(ctx, t, rank, 0);
-    DevBuf C(size_t(t->shape[p]) * rank * sizeof(double));
+    if (t->rows_only) throw InvalidArgument("the objective needs the whole tensor, not a row slab");
+    CallCache& c = call_setup(ctx, t, factors, rank, NTF_RUN_DIRECT);
     DevBuf res(sizeof(double));
-    eng.run(p, tf.dF.as<DevFactors>(), C.as<double>(), ctx->stream);
-    launch_objective(tf.dF.as<DevFactors>(), t->order, rank, p, int(t->shape[p]), C.as<double>(),
+    c.eng->run(p, c.dF.as<DevFactors>(), c.C.as<double>(), ctx->stream);
+    launch_objective(c.dF.as<DevFactors>(), t->order, rank, p, int(t->shape[p]), c.C.as<double>(),
                      t->nsq_dev.as<double>(), res.as<double>(), ctx->stream);
     NTF_CUDA(cudaMemcpyAsync(out, res.p, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
     NTF_CUDA(cudaStreamSynchronize(ctx->stream));

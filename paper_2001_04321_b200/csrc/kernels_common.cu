@@ -150,21 +150,65 @@ __global__ void sum_scratch_kernel(const double* __restrict__ scratch, int n, do
 }
 
 // Gram of one row-major rows x r matrix, ascending-row order per entry.
-__device__ void gram_rows(const double* __restrict__ a, int rows, int r, double* __restrict__ g) {
-  for (int e = threadIdx.x; e < r * r; e += blockDim.x) {
-    const int p = e / r, q = e % r;
-    double s = 0.0;
-    for (int i = 0; i < rows; ++i) s += a[(long long)i * r + p] * a[(long long)i * r + q];
-    g[e] = s;
+// g = a^T a over `rows` rows (one CTA). Thread t owns Gram entry t % r^2 of
+// row group t / r^2 (groups = blockDim / r^2 when r^2 <= blockDim) and keeps
+// four independent partial sums over its rows (no serial add chain); the
+// groups are folded in group order through `red` (>= blockDim doubles), so
+// the result is deterministic.
+__device__ void gram_rows(const double* __restrict__ a, int rows, int r, double* __restrict__ g,
+                          double* __restrict__ red) {
+  const int rr = r * r;
+  const int groups = rr <= int(blockDim.x) ? int(blockDim.x) / rr : 1;
+  for (int base = 0; base < rr; base += int(blockDim.x) / groups * 1) {
+    const int e = base + int(threadIdx.x) % (int(blockDim.x) / groups);
+    const int grp = int(threadIdx.x) / (int(blockDim.x) / groups);
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    if (e < rr && grp < groups) {
+      const int p = e / r, q = e % r;
+      int i = grp;
+      for (; i + 3 * groups < rows; i += 4 * groups) {
+        s0 += a[(long long)i * r + p] * a[(long long)i * r + q];
+        s1 += a[(long long)(i + groups) * r + p] * a[(long long)(i + groups) * r + q];
+        s2 += a[(long long)(i + 2 * groups) * r + p] * a[(long long)(i + 2 * groups) * r + q];
+        s3 += a[(long long)(i + 3 * groups) * r + p] * a[(long long)(i + 3 * groups) * r + q];
+      }
+      for (; i < rows; i += groups) s0 += a[(long long)i * r + p] * a[(long long)i * r + q];
+    }
+    red[threadIdx.x] = (s0 + s1) + (s2 + s3);
+    __syncthreads();
+    const int span = int(blockDim.x) / groups;
+    if (int(threadIdx.x) < span && base + int(threadIdx.x) < rr) {
+      double t = 0.0;
+      for (int k = 0; k < groups; ++k) t += red[k * span + threadIdx.x];
+      g[base + threadIdx.x] = t;
+    }
+    __syncthreads();
   }
 }
 
-// Grams of the X-role buffers plus the FP32 mirrors of both buffers.
-__global__ void init_factors_kernel(DevFactors* F) {
+// Fixed-order block sum of one value per thread (blockDim a power of two).
+__device__ double block_sum(double v, double* __restrict__ red) {
+  red[threadIdx.x] = v;
+  __syncthreads();
+  for (int half = int(blockDim.x) / 2; half > 0; half >>= 1) {
+    if (int(threadIdx.x) < half) red[threadIdx.x] += red[threadIdx.x + half];
+    __syncthreads();
+  }
+  const double out = red[0];
+  __syncthreads();
+  return out;
+}
+
+constexpr int kSetupThreads = 1024;
+
+// Grams of the X-role buffers plus the FP32 mirrors of both buffers; one CTA
+// per mode.
+__global__ void __launch_bounds__(kSetupThreads) init_factors_kernel(DevFactors* F) {
+  __shared__ double red[kSetupThreads];
   const int mode = blockIdx.x;
   const int rows = F->rows[mode], r = F->rank;
   const int b = F->sel[mode];
-  gram_rows(F->x[mode][b], rows, r, F->gram[mode][b]);
+  gram_rows(F->x[mode][b], rows, r, F->gram[mode][b], red);
   for (int bb = 0; bb < 2; ++bb) {
     float* m = F->x32[mode][bb];
     const double* x = F->x[mode][bb];
@@ -174,39 +218,40 @@ __global__ void init_factors_kernel(DevFactors* F) {
 }
 
 // cheap_objective at `pivot` (kernels.cpp:298-303 with the pivot of :305-311).
-__global__ void __launch_bounds__(256) objective_kernel(const DevFactors* __restrict__ F, int order, int r,
-                                                        int pivot, int rows, const double* __restrict__ C,
-                                                        const double* __restrict__ nsq,
-                                                        double* __restrict__ out) {
-  extern __shared__ double sm[];  // ga[r*r], red[256]
+__global__ void __launch_bounds__(kSetupThreads) objective_kernel(const DevFactors* __restrict__ F, int order,
+                                                                  int r, int pivot, int rows,
+                                                                  const double* __restrict__ C,
+                                                                  const double* __restrict__ nsq,
+                                                                  double* __restrict__ out) {
+  extern __shared__ double sm[];  // ga[r*r], red[blockDim]
   double* ga = sm;
   double* red = sm + r * r;
   const double* a = F->x[pivot][F->sel[pivot]];
-  gram_rows(a, rows, r, ga);
+  gram_rows(a, rows, r, ga, red);
   double cross = 0.0;
   for (long long e = threadIdx.x; e < (long long)rows * r; e += blockDim.x) cross += a[e] * C[e];
-  red[threadIdx.x] = cross;
-  __syncthreads();
-  for (int half = 128; half > 0; half >>= 1) {
-    if (threadIdx.x < half) red[threadIdx.x] += red[threadIdx.x + half];
-    __syncthreads();
+  cross = block_sum(cross, red);
+  const double* gp[kMaxOrder];
+  for (int j = 0; j < order; ++j) gp[j] = F->gram[j][F->sel[j]];
+  double quad = 0.0;
+  for (int e = threadIdx.x; e < r * r; e += blockDim.x) {
+    double g = 1.0;
+    for (int j = 0; j < order; ++j)
+      if (j != pivot) g *= gp[j][e];
+    quad += ga[e] * g;
   }
-  if (threadIdx.x == 0) {
-    double quad = 0.0;
-    for (int e = 0; e < r * r; ++e) {
-      double g = 1.0;
-      for (int j = 0; j < order; ++j)
-        if (j != pivot) g *= F->gram[j][F->sel[j]][e];
-      quad += ga[e] * g;
-    }
-    *out = 0.5 * (*nsq) - red[0] + 0.5 * quad;
-  }
+  quad = block_sum(quad, red);
+  if (threadIdx.x == 0) *out = 0.5 * (*nsq) - cross + 0.5 * quad;
 }
 
 __global__ void stamp_start_kernel(RunState* st) {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   st->t_start_ns = t;
+}
+
+__global__ void apply_time_budget_kernel(RunState* st) {
+  if (st->max_time_s > 0.0 && st->elapsed_s >= st->max_time_s) st->done = 1;
 }
 
 __global__ void compact_rows_kernel(const double* __restrict__ gathered, long long maxrows,
@@ -255,19 +300,26 @@ void launch_norm_sq(const void* t, int dtype, long long n, double* scratch, int 
 }
 
 void launch_init_factors(DevFactors* dF, const DevFactors& hF, cudaStream_t s) {
-  init_factors_kernel<<<hF.order, 256, 0, s>>>(dF);
+  init_factors_kernel<<<hF.order, kSetupThreads, 0, s>>>(dF);
   NTF_CUDA(cudaGetLastError());
 }
 
 void launch_objective(const DevFactors* dF, int order, int rank, int pivot, int rows, const double* C,
                       const double* nsq_dev, double* out, cudaStream_t s) {
-  const size_t smem = sizeof(double) * (size_t(rank) * rank + 256);
-  objective_kernel<<<1, 256, smem, s>>>(dF, order, rank, pivot, rows, C, nsq_dev, out);
+  const size_t smem = sizeof(double) * (size_t(rank) * rank + kSetupThreads);
+  if (smem > 48 * 1024)
+    NTF_CUDA(cudaFuncSetAttribute(objective_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  objective_kernel<<<1, kSetupThreads, smem, s>>>(dF, order, rank, pivot, rows, C, nsq_dev, out);
   NTF_CUDA(cudaGetLastError());
 }
 
 void launch_stamp_start(RunState* st, cudaStream_t s) {
   stamp_start_kernel<<<1, 1, 0, s>>>(st);
+  NTF_CUDA(cudaGetLastError());
+}
+
+void launch_apply_time_budget(RunState* st, cudaStream_t s) {
+  apply_time_budget_kernel<<<1, 1, 0, s>>>(st);
   NTF_CUDA(cudaGetLastError());
 }
 

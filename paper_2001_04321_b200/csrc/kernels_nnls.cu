@@ -596,7 +596,9 @@ __global__ void __launch_bounds__(TPB, 1) nnls_kernel(NnlsLaunch a) {
   a.trace[kk - 1] = rec;
   st->f_last = f;
   st->k = kk;
-  if ((st->max_iters > 0 && kk >= st->max_iters) || (st->max_time_s > 0.0 && time_s >= st->max_time_s))
+  st->elapsed_s = time_s;
+  if ((st->max_iters > 0 && kk >= st->max_iters) ||
+      (!st->collective_time && st->max_time_s > 0.0 && time_s >= st->max_time_s))
     st->done = 1;
 }
 
@@ -1312,7 +1314,9 @@ __global__ void __launch_bounds__(kStreamTPB, 1) nnls_stream_kernel(NnlsLaunch a
   a.trace[kk - 1] = rec;
   st->f_last = f;
   st->k = kk;
-  if ((st->max_iters > 0 && kk >= st->max_iters) || (st->max_time_s > 0.0 && time_s >= st->max_time_s))
+  st->elapsed_s = time_s;
+  if ((st->max_iters > 0 && kk >= st->max_iters) ||
+      (!st->collective_time && st->max_time_s > 0.0 && time_s >= st->max_time_s))
     st->done = 1;
 }
 

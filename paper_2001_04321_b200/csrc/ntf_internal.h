@@ -65,6 +65,11 @@ struct RunState {
   int k, done, max_iters, inner_max_iters;
   int algo;  // 0 = HER, 1 = AO
   int last_sweeps[kMaxOrder];
+  // multi-GPU time budget: the last-mode kernel only records its elapsed
+  // time; the ranks all-reduce (max) it and apply the budget together
+  // (launch_apply_time_budget), so every rank stops at the same iteration
+  int collective_time;
+  double elapsed_s;
 };
 
 struct TraceEntry {
@@ -118,6 +123,8 @@ void launch_init_factors(DevFactors* dF, const DevFactors& hF, cudaStream_t s);
 void launch_objective(const DevFactors* dF, int order, int rank, int pivot, int rows, const double* C,
                       const double* nsq_dev, double* out, cudaStream_t s);
 void launch_stamp_start(RunState* st, cudaStream_t s);
+// done := elapsed_s >= max_time_s (after the ranks' max-allreduce of elapsed_s)
+void launch_apply_time_budget(RunState* st, cudaStream_t s);
 void launch_compact_rows(const double* gathered, long long maxrows, const long long* begins,
                          const long long* counts, int world, int rank_cols, double* out, cudaStream_t s);
 

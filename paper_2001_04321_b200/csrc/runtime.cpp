@@ -49,15 +49,20 @@ static void nccl_check(ncclResult_t r, const char* what) {
 }
 
 void Comm::allreduce_sum(double* buf, size_t n, cudaStream_t s) const {
-  if (world == 1) return;
+  if (!nccl) return;
   nccl_check(ncclAllReduce(buf, buf, n, ncclDouble, ncclSum, static_cast<ncclComm_t>(nccl), s), "ncclAllReduce");
 }
 
 void Comm::allgather(double* buf, size_t n_per_rank, cudaStream_t s) const {
-  if (world == 1) return;
+  if (!nccl) return;
   nccl_check(ncclAllGather(buf + size_t(rank) * n_per_rank, buf, n_per_rank, ncclDouble,
                            static_cast<ncclComm_t>(nccl), s),
              "ncclAllGather");
+}
+
+void Comm::allreduce_max(double* buf, size_t n, cudaStream_t s) const {
+  if (!nccl) return;
+  nccl_check(ncclAllReduce(buf, buf, n, ncclDouble, ncclMax, static_cast<ncclComm_t>(nccl), s), "ncclAllReduce(max)");
 }
 
 Comm::~Comm() {
@@ -109,7 +114,8 @@ MttkrpEngine::MttkrpEngine(const ntf_ctx* ctx, const ntf_tensor* t, int rank, un
     need = std::max(need, size_t(segs) * size_t(v.I) * rank);
     need = std::max(need, fast_mttkrp_partial_len(v, t->dtype, ctx->sms));
   }
-  if ((flags & NTF_RUN_DIMTREE) && !(flags & NTF_RUN_GENERIC) && t->order >= 3 &&
+  // the dimension tree is the default; NTF_RUN_DIRECT asks for N full passes
+  if (!(flags & (NTF_RUN_DIRECT | NTF_RUN_GENERIC)) && t->order >= 3 &&
       view(t->order - 1).L < (1LL << 31)) {
     // Split point h of the dimension tree: blocks 0..h-1 contract
     // Y_L = T x_h A_h ... x_{N-1} A_{N-1} (previous sweep), blocks h..N-1
@@ -205,7 +211,7 @@ MttkrpEngine::MttkrpEngine(const ntf_ctx* ctx, const ntf_tensor* t, int rank, un
       unit_tab_[m] = DevBuf(tab.size() * sizeof(int));
       NTF_CUDA(cudaMemcpy(unit_tab_[m].p, tab.data(), tab.size() * sizeof(int), cudaMemcpyHostToDevice));
     }
-  if (ctx->comm.world > 1) {
+  if (ctx->comm.active()) {
     const int world = ctx->comm.world;
     std::vector<long long> meta(static_cast<size_t>(2 * world));
     for (int p = 0; p < world; ++p) {
@@ -269,8 +275,12 @@ void MttkrpEngine::run(int mode, const DevFactors* dF, double* out, cudaStream_t
                        cudaEvent_t ev1) {
   const ModeView v = view(mode);
   const Comm& comm = ctx_->comm;
-  const bool gather = comm.world > 1 && mode == 0;
+  const bool gather = comm.active() && mode == 0;
   double* dst = gather ? gather_.as<double>() + size_t(comm.rank) * maxrows_ * rank_ : out;
+  if (t_->rows_only && mode == 0) {  // a row slab on one GPU: its rows of the full I_1 x r output
+    NTF_CUDA(cudaMemsetAsync(out, 0, size_t(t_->shape[0]) * rank_ * sizeof(double), s));
+    dst = out + size_t(t_->row0) * rank_;
+  }
   const bool seq = last_mode_ == mode - 1;
   last_mode_ = mode;
   if (ev0) NTF_CUDA(cudaEventRecord(ev0, s));
@@ -306,7 +316,7 @@ void MttkrpEngine::run(int mode, const DevFactors* dF, double* out, cudaStream_t
     if (ev1) NTF_CUDA(cudaEventRecord(ev1, s));
     launch_reduce_partials(partial_.as<double>(), segs_[mode], v.I * rank_, dst, s);
   }
-  if (comm.world == 1) return;
+  if (!comm.active()) return;
   if (gather) {
     comm.allgather(gather_.as<double>(), size_t(maxrows_) * rank_, s);
     const long long* meta = slab_meta_.as<long long>();
@@ -324,6 +334,8 @@ constexpr int kNnlsScratch = 3072 + 64 * kMaxRank * kMaxRank;
 Session::Session(ntf_ctx* ctx, const ntf_tensor* t, int algo, const double* init, int rank,
                  const ntf_ao_config& cfg, const ntf_her_params* params)
     : ctx_(ctx), t_(t), algo_(algo), rank_(rank), order_(t->order), cfg_(cfg) {
+  if (t->rows_only)
+    throw InvalidArgument("a row-slab tensor of a 1-GPU context serves MTTKRP calls only, not solver runs");
   static const bool timing = std::getenv("NTF_TIMING") != nullptr;
   const auto now = [] { return std::chrono::steady_clock::now(); };
   const auto t0 = now();
@@ -383,6 +395,8 @@ Session::Session(ntf_ctx* ctx, const ntf_tensor* t, int algo, const double* init
   st.inner_max_iters = cfg.inner_stop.max_iters;
   st.tol = cfg.inner_stop.rel_change_tol;
   st.algo = algo;
+  collective_time_ = ctx->comm.active() && cfg.max_time_s > 0.0;
+  st.collective_time = collective_time_ ? 1 : 0;
   NTF_CUDA(cudaMemcpyAsync(state_.p, &st, sizeof st, cudaMemcpyHostToDevice, stream_));
 
   // GramCache::create + pivot objective f0 (driver_common.hpp:50-56), then
@@ -441,6 +455,10 @@ void Session::enqueue_iteration(bool timed) {
     a.bufs = hF_;
     a.has_bufs = 1;
     launch_nnls(a, stream_);
+  }
+  if (collective_time_) {  // every rank applies the same (max) elapsed time
+    ctx_->comm.allreduce_max(&st->elapsed_s, 1, stream_);
+    launch_apply_time_budget(st, stream_);
   }
 }
 
@@ -550,6 +568,29 @@ void Session::trace(double* f0, ntf_trace_record* out, int cap, int* n) {
     }
     out[i] = r;
   }
+}
+
+bool Session::last_record(ntf_trace_record* out) {
+  RunState st;
+  NTF_CUDA(cudaMemcpyAsync(&st, state_.p, sizeof st, cudaMemcpyDeviceToHost, stream_));
+  sync();
+  if (st.k <= 0 || st.k > trace_cap_) return false;
+  TraceEntry e;
+  NTF_CUDA(cudaMemcpyAsync(&e, trace_.as<TraceEntry>() + (st.k - 1), sizeof e, cudaMemcpyDeviceToHost, stream_));
+  sync();
+  ntf_trace_record r{};
+  r.iter = st.k;
+  r.time_s = e.time_s;
+  r.f = e.f;
+  r.inner_sweeps = e.sweeps;
+  if (algo_ == 0) {
+    r.has_restarted = 1;
+    r.restarted = e.restarted;
+    r.has_beta = 1;
+    r.beta = e.beta;
+  }
+  *out = r;
+  return true;
 }
 
 void Session::set_kernel_timing(bool on) { timing_ = on; }

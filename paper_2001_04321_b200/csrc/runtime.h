@@ -54,8 +54,12 @@ struct DevBuf {
 struct Comm {
   void* nccl = nullptr;  // ncclComm_t
   int rank = 0, world = 1;
+  // collectives run whenever a communicator exists -- also for a 1-rank
+  // world created through ntf_ctx_create_dist (the NCCL path on one GPU)
+  bool active() const { return nccl != nullptr; }
   void allreduce_sum(double* buf, size_t n, cudaStream_t s) const;
   void allgather(double* buf, size_t n_per_rank, cudaStream_t s) const;  // in place
+  void allreduce_max(double* buf, size_t n, cudaStream_t s) const;
   ~Comm();
 };
 
@@ -109,6 +113,17 @@ class MttkrpEngine {
   TreeView tree_view(int mode) const;
 };
 
+// Per-tensor workspace of the per-call provider entry points (ntf_mttkrp,
+// ntf_mttkrp_all, ntf_objective): the engine (unit tables, partial slabs) and
+// the factor buffers of the last (rank, flags), reused while they match.
+struct CallCache {
+  int rank = 0;
+  unsigned flags = 0;
+  std::unique_ptr<MttkrpEngine> eng;
+  DevBuf fac, fac32, grams, dF, C;
+  DevFactors h{};
+};
+
 // ---- GPU-resident solver session ---------------------------------------------
 class Session {
  public:
@@ -121,6 +136,7 @@ class Session {
   bool done();
   void factors(double* out);
   void trace(double* f0, ntf_trace_record* out, int cap, int* n);
+  bool last_record(ntf_trace_record* out);  // the newest trace record (false: none yet)
   void set_kernel_timing(bool on);
   void kernel_times(double* ms_per_mode, int* launches, int* total_kernels);
   cudaStream_t stream() const { return stream_; }
@@ -151,6 +167,7 @@ class Session {
   int kernel_n_[kMaxOrder] = {};
   int host_iters_ = 0;  // iterations enqueued
   int done_host_ = 0;  // host mirror of RunState::done
+  bool collective_time_ = false;  // a communicator and a time budget
 };
 
 }  // namespace ntfb
@@ -175,4 +192,6 @@ struct ntf_tensor {
   ntfb::DevBuf data;
   ntfb::DevBuf nsq_dev;  // ||T||^2 (global, FP64) on the device
   double nsq = 0.0;
+  bool rows_only = false;  // a caller-chosen row slab on a 1-GPU context (ntf_tensor_upload_rows)
+  mutable std::unique_ptr<ntfb::CallCache> cache;
 };

@@ -71,7 +71,7 @@ def test_dimtree_ao_trace_parity(P, oracle, shape, rank, sigma, seed):
 def test_dimtree_matches_direct_at_full_size(P, shape, rank):
     t, truth, init = _instance(P, shape, rank, 0.01, 102)
     prov = P.GpuDenseProvider(t)
-    _, direct = P.her_run(prov, init, P.AoConfig(max_outer_iters=8), P.HerParams())
+    _, direct = P.her_run(prov, init, P.AoConfig(max_outer_iters=8, flags=P.RUN_DIRECT), P.HerParams())
     _, tree = P.her_run(prov, init, P.AoConfig(max_outer_iters=8, flags=P.RUN_DIMTREE), P.HerParams())
     assert abs(direct.f0 - tree.f0) <= 1e-14 * abs(direct.f0)
     for a, b in zip(direct.records, tree.records):
@@ -93,7 +93,7 @@ def test_dimtree_f32_ao_trace(P, oracle, shape, rank):
     prov = P.GpuDenseProvider(t)
     nsq = prov.norm_sq()
     _, tree = P.ao_run(prov, init, P.AoConfig(max_outer_iters=20, flags=P.RUN_DIMTREE))
-    _, direct = P.ao_run(prov, init, P.AoConfig(max_outer_iters=20))
+    _, direct = P.ao_run(prov, init, P.AoConfig(max_outer_iters=20, flags=P.RUN_DIRECT))
     t64 = np.asarray(t, dtype=np.float64)
     _, f0, recs = oracle.run("ao", t64, init.factors, max_outer_iters=20)
     dev_o = max(abs(a.f - w["f"]) for a, w in zip(tree.records, recs)) / nsq
