@@ -143,6 +143,11 @@ static void check_model(const std::vector<int>& shape, const Model& m) {
 // Dense MTTKRP in the reference's loop order (src/kernels.cpp:161-191):
 // per output row `mid`, for each `left`: inner = sum_right T * wr[right,:]
 // (ascending right), then acc += wl[left,:] .* inner.
+// Summation-order variant (conditioning experiments only, tools/r02/
+// oracle_sensitivity.py): 1 walks `left` and `right` in descending order -- the
+// same algorithm, rounded differently. 0 (default) is the reference's order.
+int g_sum_order = 0;
+
 template <typename T>
 Mat mttkrp(const T* data, const std::vector<int>& shape, const Model& m, int mode) {
   check_model(shape, m);
@@ -158,10 +163,12 @@ Mat mttkrp(const T* data, const std::vector<int>& shape, const Model& m, int mod
 #pragma omp parallel for schedule(static)
   for (int64_t mid = 0; mid < s.mid; ++mid) {
     std::vector<double> acc(static_cast<size_t>(r), 0.0), inner(static_cast<size_t>(r));
-    for (int64_t left = 0; left < s.left; ++left) {
+    for (int64_t li = 0; li < s.left; ++li) {
+      const int64_t left = g_sum_order ? s.left - 1 - li : li;
       const T* src = data + (left * s.mid + mid) * s.right;
       std::fill(inner.begin(), inner.end(), 0.0);
-      for (int64_t right = 0; right < s.right; ++right) {
+      for (int64_t ri = 0; ri < s.right; ++ri) {
+        const int64_t right = g_sum_order ? s.right - 1 - ri : ri;
         const double t = double(src[right]);
         const double* w = &wr.v[size_t(right * r)];
         for (int64_t c = 0; c < r; ++c) inner[size_t(c)] += t * w[c];

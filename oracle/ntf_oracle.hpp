@@ -63,6 +63,7 @@ Split split_around(const std::vector<int>& shape, int mode);
 Mat khatri_rao(const std::vector<const Mat*>& ms);
 template <typename T>
 Mat mttkrp(const T* data, const std::vector<int>& shape, const Model& m, int mode);
+extern int g_sum_order;  // 0 = reference order; 1 = descending (conditioning experiments)
 Mat gram(const Mat& a);
 Mat hadamard_of_grams(const std::vector<Mat>& grams, int skip);
 double cheap_objective(double norm_sq, const Mat& a, const Mat& g, const Mat& c);

@@ -279,3 +279,7 @@ extern "C" int ora_set_threads(int n) {
   if (n > 0) omp_set_num_threads(n);
   return prev;
 }
+
+// MTTKRP summation order (0 = the reference's, 1 = descending): conditioning
+// experiments only (tools/r02/oracle_sensitivity.py).
+extern "C" void ora_set_sum_order(int order) { ora::g_sum_order = order; }

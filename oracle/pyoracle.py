@@ -92,6 +92,12 @@ def _split(flat, shape, rank):
     return out
 
 
+def set_sum_order(order):
+    """MTTKRP summation order: 0 = the reference's, 1 = descending (same
+    algorithm, different rounding; conditioning experiments only)."""
+    lib().ora_set_sum_order(int(order))
+
+
 def set_threads(n):
     """OpenMP threads of the oracle's parallel loops; returns the previous maximum."""
     return int(lib().ora_set_threads(int(n)))

@@ -93,6 +93,14 @@ void check_run_inputs(const ntf_tensor* t, const double* init, int rank, const n
   if (cfg.solver != NTF_SOLVER_AHALS)
     throw Unsupported("only the AHALS inner solver runs on the GPU path");
   if (cfg.inner_stop.max_iters < 0) throw InvalidArgument("inner max_iters must be >= 0");
+  // the fused block update keeps a factor on one thread-block cluster
+  // (launch_nnls): refuse up front, before the session is built
+  if (rank > kMaxRank) throw Unsupported("rank above the fused NNLS kernel's limit (64)");
+  for (int i = 0; i < t->order; ++i)
+    if (t->shape[i] > kMaxNnlsRows)
+      throw Unsupported("mode " + std::to_string(i) + " has " + std::to_string(t->shape[i]) +
+                        " rows; the fused NNLS kernel holds at most " + std::to_string(kMaxNnlsRows) +
+                        " rows per factor");
 }
 
 // The tensor handle of this rank's mode-1 slab; `fill` copies the slab's

@@ -887,6 +887,7 @@ __global__ void __launch_bounds__(kStreamTPB, 1) nnls_stream_kernel(NnlsLaunch a
   const long long t_loop = clock64();
 
   const int warp = int(threadIdx.x >> 5), lane = int(threadIdx.x & 31);
+  int red_np = 0, red_nd = -1;  // reducer: sweeps posted / the deciding sweep (for the drain)
   if (warp < nrw) {
     // ------------------------------------------------------------ row warps
     const int slot = (warp * 32 + lane) / Q, k = lane % Q, gbase = lane & ~(Q - 1);
@@ -1098,14 +1099,50 @@ __global__ void __launch_bounds__(kStreamTPB, 1) nnls_stream_kernel(NnlsLaunch a
             const unsigned long long w = (stop ? (1ull << 32) : 0ull) | unsigned(nd + 1);
             asm volatile("st.volatile.shared.u64 [%0], %1;" ::"r"(smem_u32(ctl)), "l"(w) : "memory");
           }
-          if (stop) break;
+          if (stop) {
+            red_nd = nd;
+            break;
+          }
           ++nd;
           idle = false;
         }
         if (idle) __nanosleep(64);
       }
+      red_np = np;
     }
   }
+  // Before the last cluster barrier every st.async aimed at this CTA must
+  // have landed (no CTA may leave while traffic can still target its shared
+  // memory). Rows run at most D - 1 sweeps past the decisions, so reducers
+  // posted sweeps <= red_nd + D - 1 at most, each CTA its own count. The
+  // reducer posts zeros for the sweeps it has not posted up to that bound
+  // (arming its own ring slot each time), so every slot phase up to it gets
+  // exactly one post from every CTA, then waits for those phases. (The rows'
+  // st.async into their own CTA's ring come from threads of this CTA, which
+  // are all behind the final barrier.)
+  auto drain = [&]() {
+    if (warp != nrw || max_iters <= 0 || red_nd < 0) return;
+    const int last = min(red_nd + D - 1, max_iters - 1);
+    for (int x = red_np; x <= last; ++x) {
+      const int cb = x % kStreamDC;
+      if (lane == 0)
+        asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&cbar[cb])),
+                     "r"(ncta * 8u)
+                     : "memory");
+      if (unsigned(lane) < ncta) {
+        uint32_t raddr, rbar;
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
+                     : "=r"(raddr)
+                     : "r"(smem_u32(&cslot[cb * kMaxCluster + me])), "r"(lane));
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rbar) : "r"(smem_u32(&cbar[cb])), "r"(lane));
+        asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(raddr),
+                     "l"(0ll), "r"(rbar)
+                     : "memory");
+      }
+    }
+    for (int x = red_nd + 1; x <= last; ++x)
+      while (!mbar_test(&cbar[x % kStreamDC], uint32_t(x / kStreamDC) & 1u)) __nanosleep(32);
+  };
   __syncthreads();
   const long long t_loop_end = clock64();
   const int s = int(*ctl & 0xffffffffu);  // sweeps run (nnls.cpp:31-45)
@@ -1118,6 +1155,7 @@ __global__ void __launch_bounds__(kStreamTPB, 1) nnls_stream_kernel(NnlsLaunch a
       if (i < rpc && row < a.rows && l < r) a.w_out[(long long)row * r + l] = stash[(fs * nloc + i) * LDW + l];
     }
     if (blockIdx.x == 0 && threadIdx.x == 0 && a.sweeps_out) *a.sweeps_out = s;
+    drain();
     cl.sync();  // no CTA leaves while cluster traffic may target it
     return;
   }
@@ -1258,7 +1296,8 @@ __global__ void __launch_bounds__(kStreamTPB, 1) nnls_stream_kernel(NnlsLaunch a
       }
   }
   const long long t_e4 = clock64();
-  cl.sync();  // remote reads done before any CTA exits
+  drain();
+  cl.sync();  // remote reads and every cluster post done before any CTA exits
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     const long long t_end = clock64();
     unsigned long long* ph = &g_nnls_skew[2][64];  // phase cycles (diagnostics)
@@ -1404,7 +1443,7 @@ void launch_nnls(const NnlsLaunch& a, cudaStream_t s) {
   const int r = a.rank;
   if (r < 1 || r > kMaxRank) throw Unsupported("rank outside the fused NNLS kernel's range (1..64)");
   if (launch_stream(a, s)) return;
-  if (a.rows > kMaxCluster * 256) throw Unsupported("factor taller than 4096 rows");
+  if (a.rows > kMaxNnlsRows) throw Unsupported("factor taller than 4096 rows");
   if (r <= 4) return launch_rp<4, 256>(a, s);
   if (r <= 8) return launch_rp<8, 256>(a, s);
   if (r <= 12) return launch_rp<12, 256>(a, s);

@@ -12,27 +12,43 @@ make_config_golden.py); the instances are regenerated here by the host
 generator, which is bit-identical to the oracle's (test_host_api.py), and
 their fingerprint (||T||^2, first/last entries) is checked first.
 
-Bars:
-  * FP64 (c2, c3): |f_k - f_k^ora| <= 1e-8 |f_k^ora| + 64 eps ||T||^2
-    (tests/parity.py: the cancellation floor of the cheap objective),
-    identical restart decisions wherever |F_k - F_{k-1}| exceeds that floor,
-    beta_k to 1e-12; final factors 1e-6 relative Frobenius; e_50 (metrics.cpp:
-    79-111) within 1e-6 relative.
-  * FP32 (c4): the kernels multiply in FP32 (per-call MTTKRP bar 1e-5), so
-    f_k carries FP32 rounding of <A, C> ~ 1e-7 ||T||^2: |f_k - f_k^ora| <=
-    1e-6 ||T||^2, restart decisions identical wherever |F_k - F_{k-1}| > 4e-6
-    ||T||^2 (beyond the combined error of two evaluations), e_50 within 1e-2
-    relative.
+Bars (the measurements behind them: tools/r02/oracle_sensitivity.py and
+tests/golden/make_exact_f0.py, numbers in DESIGN.md §4):
+  * f0 (FP64): the reference's sequential sums are themselves off by up to
+    1.4e-12 relative at these sizes (the oracle's f0 against an
+    extended-precision evaluation, tests/golden/config_f0_exact.json), so the
+    GPU f0 is held to 1e-12 relative against the EXACT value, and to 1e-12
+    plus the oracle's own measured error against the oracle.
+  * f_k (FP64, c2, c3): |f_k - f_k^ora| <= 1e-8 |f_k^ora| + 256 eps ||T||^2.
+    Two faithful FP64 runs drift apart: the oracle with its MTTKRP summed in
+    descending order deviates from itself by up to 1170 eps ||T||^2 (c3) and
+    by 1e-4 relative once f_k nears the ||T||^2 cancellation floor (c2, a
+    noiseless instance converging to f ~ 1e-10 ||T||^2); 256 eps is the floor
+    the production path needs (167 eps at c2), the relative term is the north
+    star's. Restart decisions identical wherever |F_k - F_{k-1}| exceeds four
+    floors, beta_k to 1e-12; final factors 1e-6 relative Frobenius; e_50
+    (metrics.cpp:79-111) within 1e-6 relative.
+  * FP32 (c4): the kernels multiply in FP32 with FP32 factor mirrors (per-call
+    MTTKRP bar 1e-5), so f_k carries ~1e-8 ||T||^2 of rounding of <A, C>:
+    |f_k - f_k^ora| <= 1e-6 ||T||^2, restart decisions identical wherever
+    |F_k - F_{k-1}| > 4e-6 ||T||^2, e_50 within 1e-2 relative.
 """
+import json
 import os
 
 import numpy as np
 import pytest
 
-from parity import F_FLOOR, rel_fro
+from parity import rel_fro
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CONFIGS = ["c2", "c3", "c4"]
+CONFIG_FLOOR = 256 * 2.0 ** -52  # absolute f_k floor in units of ||T||^2 (see the module docstring)
+
+
+def _exact_f0(name):
+    with open(os.path.join(HERE, "golden", "config_f0_exact.json")) as fh:
+        return json.load(fh)[name]
 
 
 def _fixture(name):
@@ -59,6 +75,15 @@ def instances(P):
     return get
 
 
+def _report(rep):
+    """NTF_PARITY_REPORT=<dir>: every run's deviation profile as JSON lines."""
+    d = os.environ.get("NTF_PARITY_REPORT")
+    if d:
+        os.makedirs(d, exist_ok=True)
+        with open(os.path.join(d, "config_parity.jsonl"), "a") as fh:
+            fh.write(json.dumps(rep) + "\n")
+
+
 def test_config_fixtures_cover_the_north_star_configs():
     for name in CONFIGS:
         g = _fixture(name)
@@ -67,6 +92,10 @@ def test_config_fixtures_cover_the_north_star_configs():
         assert g["her_restarted"].dtype == bool
         assert np.all(np.diff(g["ao_f"]) <= 1e-12 * float(g["ao_f0"]))  # AO is monotone (test_ao.cpp:83-104)
     assert bool(_fixture("c4")["collinear"]) and str(_fixture("c4")["dtype"]) == "f32"
+    for name in CONFIGS:  # the extended-precision f0 belongs to the same instance and init
+        ex = _exact_f0(name)
+        assert ex["oracle_f0"] == float(_fixture(name)["her_f0"]) == float(_fixture(name)["ao_f0"])
+        assert abs(ex["oracle_f0"] - ex["f0_exact"]) <= 2e-11 * abs(ex["f0_exact"])
 
 
 @pytest.mark.gpu
@@ -91,20 +120,35 @@ def test_config_trace_parity(P, instances, name, algo):
     fo = g[f"{algo}_f"]
     fp32 = str(g["dtype"]) == "f32"
     assert len(trace.records) == 50
+    fg = np.array([rec.f for rec in trace.records])
+    assert [rec.iter for rec in trace.records] == list(range(1, 51))
+    e_gpu = P.factor_error(model, truth)
+    e_ora = float(g[f"{algo}_e"])
+    finals = [g[f"{algo}_final{i}"] for i in range(len(init.factors))]
+    report = {"config": name, "algo": algo, "f0_rel": abs(trace.f0 - f0o) / abs(f0o),
+              "f_rel": (np.abs(fg - fo) / np.abs(fo)).tolist(), "f_abs_over_nsq": (np.abs(fg - fo) / nsq).tolist(),
+              "e_gpu": e_gpu, "e_oracle": e_ora, "final_rel_fro": [rel_fro(a, b) for a, b in zip(model, finals)]}
+    if algo == "her":
+        report["restart_gpu"] = [bool(rec.restarted) for rec in trace.records]
+        report["restart_oracle"] = [bool(x) for x in g["her_restarted"]]
+    if not fp32:
+        report["f0_rel_exact"] = abs(trace.f0 - _exact_f0(name)["f0_exact"]) / abs(_exact_f0(name)["f0_exact"])
+    _report(report)
+    floor = CONFIG_FLOOR * nsq
     if fp32:
         bar = lambda ref: 1e-6 * nsq  # noqa: E731
         decision_floor = 4e-6 * nsq
+        assert abs(trace.f0 - f0o) <= 1e-6 * nsq, (trace.f0, f0o)
     else:
-        bar = lambda ref: 1e-8 * abs(ref) + F_FLOOR * nsq  # noqa: E731
-        decision_floor = 4 * F_FLOOR * nsq
-    assert abs(trace.f0 - f0o) <= (1e-6 * nsq if fp32 else 1e-12 * abs(f0o) + F_FLOOR * nsq), (trace.f0, f0o)
-    worst = 0.0
+        bar = lambda ref: 1e-8 * abs(ref) + floor  # noqa: E731
+        decision_floor = 4 * floor
+        ex = _exact_f0(name)
+        assert abs(trace.f0 - ex["f0_exact"]) <= 1e-12 * abs(ex["f0_exact"]), (trace.f0, ex)
+        assert abs(trace.f0 - f0o) <= 1e-12 * abs(f0o) + abs(f0o - ex["f0_exact"]), (trace.f0, f0o, ex)
     decided = 0
     prev = f0o
     for k, rec in enumerate(trace.records):
-        assert rec.iter == k + 1
         dev = abs(rec.f - fo[k])
-        worst = max(worst, dev / abs(fo[k]))
         assert dev <= bar(fo[k]), f"{name} {algo} iter {k + 1}: gpu {rec.f!r} oracle {fo[k]!r}"
         if algo == "her" and abs(fo[k] - prev) > decision_floor:
             decided += 1
@@ -113,12 +157,9 @@ def test_config_trace_parity(P, instances, name, algo):
                 assert abs(rec.beta - g["her_beta"][k]) <= 1e-12 * abs(g["her_beta"][k])
         prev = fo[k]
     if algo == "her":
-        assert decided >= 40, decided  # the decisions really were compared
-    finals = [g[f"{algo}_final{i}"] for i in range(len(init.factors))]
+        # the decisions really were compared (FP32: only the steps beyond its 4e-6 ||T||^2 floor)
+        assert decided >= (10 if fp32 else 40), decided
     if not fp32:
         for a, b in zip(model, finals):
             assert rel_fro(a, b) < 1e-6
-    e_gpu = P.factor_error(model, truth)
-    e_ora = float(g[f"{algo}_e"])
     assert abs(e_gpu - e_ora) <= (1e-2 if fp32 else 1e-6) * e_ora, (e_gpu, e_ora)
-    print(f"{name} {algo}: worst rel f dev {worst:.2e}, decisions compared {decided}, e {e_gpu:.6e} vs {e_ora:.6e}")

@@ -290,3 +290,35 @@ def test_driver_validation(P):
         P.her_run(t, bad, P.AoConfig(max_outer_iters=3))
     with pytest.raises(P.UnsupportedError):
         P.her_run(t, init, P.AoConfig(solver=P.NnlsSolver.admm, max_outer_iters=3))
+
+
+def test_too_tall_factor_is_refused_up_front(P):
+    """The fused block update holds a factor on one 16-CTA cluster (4096 rows,
+    r <= 64): such runs fail before the session is built (ntf_her_run)."""
+    t, _, init = _instance(P, [5000, 2, 2], 1, 0.0, 1)
+    with pytest.raises(P.UnsupportedError, match="4096"):
+        P.her_run(t, init, P.AoConfig(max_outer_iters=2))
+
+
+@pytest.mark.parametrize("shape,rank,dtype", [([120, 100, 80], 20, np.float64), ([40, 36, 34, 32], 16, np.float64),
+                                              ([96, 80, 64], 32, np.float32)], ids=["3way-f64", "4way-f64", "3way-f32"])
+def test_production_path_is_bitwise_deterministic(P, shape, rank, dtype):
+    """test_her.cpp:251-271 on the production kernels (TMA/DMMA or FFMA
+    MTTKRP with the in-kernel split-K grid barrier, tree contractions with
+    self-resetting arrival counters, the stream NNLS with its st.async
+    cluster exchange, graph replay): two runs from identical inputs give
+    identical bits -- in traces, decisions and factors. compute-sanitizer is
+    not available on the GPU pool (runs under it are refused), so this and
+    the oracle parity are the race evidence."""
+    spec = P.SyntheticSpec(shape=shape, rank=rank, noise_sigma=0.01, seed=61)
+    t, _ = P.generate(spec, dtype=dtype)
+    init = P.random_init(shape, rank, P.stream_seed(61, 1))
+    prov = P.GpuDenseProvider(t)
+    runs = [P.her_run(prov, init, P.AoConfig(max_outer_iters=30), P.HerParams()) for _ in range(2)]
+    (ma, ta), (mb, tb) = runs
+    assert ta.f0 == tb.f0
+    assert [(r.f, r.beta, r.restarted, r.inner_sweeps) for r in ta.records] == \
+        [(r.f, r.beta, r.restarted, r.inner_sweeps) for r in tb.records]
+    for a, b in zip(ma, mb):
+        assert np.array_equal(a, b)
+    prov.close()
