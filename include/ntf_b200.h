@@ -219,6 +219,30 @@ int ntf_tensor_destroy(ntf_tensor* t);
  * rank's mode-1 slab is read (one seek) and streamed to the device through
  * pinned staging buffers, rounded to FP32 when dtype is NTF_DTYPE_F32. */
 int ntf_tensor_upload_ntft(ntf_ctx* ctx, const char* path, int dtype, ntf_tensor** out);
+/* TuckerProvider (include/ntf/tucker.hpp:60-73, src/tucker.cpp:62-77, 94-95):
+ * a TuckerFormat -- the dense core (order N, dims core_shape, row-major) and
+ * one basis per mode, U_l (full_shape[l] x core_shape[l], row-major,
+ * orthonormal columns), concatenated in mode order -- as a provider handle.
+ * ntf_mttkrp / ntf_mttkrp_all / ntf_objective / the drivers accept it; the
+ * MTTKRP runs in the compressed space (P_l = U_l^T A_l, the core's MTTKRP
+ * with P on the dense kernels, then U_mode times it) and ||T||^2 is
+ * ||core||^2. Validation as TuckerFormat::validate (tucker.cpp:16-26):
+ * NTF_ERR_INVALID_ARGUMENT "basis columns are not orthonormal" (|U^T U - I|
+ * > 1e-10), "basis column count does not match the core shape". One GPU
+ * (NTF_ERR_UNSUPPORTED on an NCCL context). */
+int ntf_tucker_upload(ntf_ctx* ctx, const double* core, int order, const int64_t* core_shape,
+                      const double* bases, const int64_t* full_shape, ntf_tensor** out);
+/* TuckerFormat::save / load (tucker.cpp:106-165): container "NTFK" (magic,
+ * u32 version 1, u32 order, u64 full dims, u64 core dims, FP64 core, the
+ * bases row-major in mode order). info: order and both shapes; read: core
+ * and concatenated bases into caller buffers. Errors as TuckerFormat::load
+ * (NTF_ERR_RUNTIME: "cannot open", "not a tucker container", "unsupported
+ * version", "bad order", "truncated payload"). */
+int ntf_ntfk_info(const char* path, int* order, int64_t* full_shape, int64_t* core_shape);
+int ntf_ntfk_read(const char* path, double* core, double* bases);
+int ntf_ntfk_write(const char* path, const double* core, const double* bases, int order,
+                   const int64_t* full_shape, const int64_t* core_shape);
+int ntf_tensor_upload_ntfk(ntf_ctx* ctx, const char* path, ntf_tensor** out);
 /* ObjectiveProvider::mttkrp (provider.hpp:18; kernels.cpp:161-191): out is
  * the I_mode x rank MTTKRP (row-major, FP64), identical on every rank. The
  * tensor keeps the kernel plan and device workspaces of its last (rank)

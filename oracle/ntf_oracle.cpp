@@ -645,4 +645,41 @@ double factor_error(const Model& est, const Model& truth) {
   return err / n;
 }
 
+// compressed_mttkrp (tucker.cpp:62-77): project every other factor into the
+// compressed space (P_l = U_l^T A_l), contract the core with their
+// Khatri-Rao product -- the reference's unfold(core, mode) * khatri_rao(P)
+// with its ordering convention is the MTTKRP of the core with the P_l
+// (kernels.cpp:161-191; the reference pins compressed == dense MTTKRP in
+// test_tucker.cpp:71-99) -- then U_mode times it.
+Mat compressed_mttkrp(const double* core, const std::vector<int>& core_shape, const std::vector<Mat>& bases,
+                      const Model& m, int mode) {
+  const int n = int(m.size());
+  if (int(bases.size()) != n || int(core_shape.size()) != n)
+    throw std::invalid_argument("compressed_mttkrp: order mismatch");
+  const int64_t r = m[0].cols;
+  Model proj;
+  for (int l = 0; l < n; ++l) {
+    const Mat& u = bases[size_t(l)];
+    Mat pl(u.cols, r);
+    if (l != mode)
+      for (int64_t a = 0; a < u.cols; ++a)
+        for (int64_t c = 0; c < r; ++c) {
+          double acc = 0.0;
+          for (int64_t i = 0; i < u.rows; ++i) acc += u(i, a) * m[size_t(l)](i, c);
+          pl(a, c) = acc;
+        }
+    proj.push_back(pl);
+  }
+  const Mat mc = mttkrp(core, core_shape, proj, mode);
+  const Mat& um = bases[size_t(mode)];
+  Mat out(um.rows, r);
+  for (int64_t i = 0; i < um.rows; ++i)
+    for (int64_t c = 0; c < r; ++c) {
+      double acc = 0.0;
+      for (int64_t a = 0; a < um.cols; ++a) acc += um(i, a) * mc(a, c);
+      out(i, c) = acc;
+    }
+  return out;
+}
+
 }  // namespace ora

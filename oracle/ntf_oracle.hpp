@@ -116,6 +116,11 @@ Model ao_run(const T* data, const std::vector<int>& shape, const Model& init, co
              RunTrace& trace);
 
 // ---- metrics (metrics.cpp:10-111) ------------------------------------------
+// ---- TuckerProvider (tucker.hpp:60-73, tucker.cpp:62-77) -------------------
+// U_mode * MTTKRP(core, {U_l^T A_l}_l, mode); bases[l] is I_l x r_l.
+Mat compressed_mttkrp(const double* core, const std::vector<int>& core_shape, const std::vector<Mat>& bases,
+                      const Model& m, int mode);
+
 Mat normalize_columns(const Mat& a);
 std::vector<int> hungarian(const Mat& cost, double* cost_out);
 double factor_error(const Model& est, const Model& truth);

@@ -283,3 +283,30 @@ extern "C" int ora_set_threads(int n) {
 // MTTKRP summation order (0 = the reference's, 1 = descending): conditioning
 // experiments only (tools/r02/oracle_sensitivity.py).
 extern "C" void ora_set_sum_order(int order) { ora::g_sum_order = order; }
+
+// compressed_mttkrp (tucker.cpp:62-77): core row-major (core_shape), bases
+// concatenated row-major (full_shape[l] x core_shape[l]), factors as usual.
+extern "C" int ora_compressed_mttkrp(const double* core, const int* core_shape, const double* bases,
+                                     const int* full_shape, int order, const double* factors, int rank, int mode,
+                                     double* out) {
+  try {
+    std::vector<ora::Mat> bs;
+    size_t off = 0;
+    for (int l = 0; l < order; ++l) {
+      ora::Mat b(full_shape[l], core_shape[l]);
+      std::memcpy(b.v.data(), bases + off, b.v.size() * sizeof(double));
+      off += b.v.size();
+      bs.push_back(std::move(b));
+    }
+    const ora::Model m = unpack(factors, full_shape, order, rank);
+    const ora::Mat c = ora::compressed_mttkrp(core, std::vector<int>(core_shape, core_shape + order), bs, m, mode);
+    std::memcpy(out, c.v.data(), c.v.size() * sizeof(double));
+    return 0;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return 1;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 2;
+  }
+}

@@ -157,6 +157,19 @@ def mttkrp(tensor, model, mode):
     return out
 
 
+def compressed_mttkrp(core, bases, model, mode):
+    """tucker.cpp:62-77 (core: ndarray, bases: list of I_l x r_l)."""
+    core = np.ascontiguousarray(core, np.float64)
+    order = core.ndim
+    rank = model[0].shape[1]
+    full = [b.shape[0] for b in bases]
+    flat_b = np.ascontiguousarray(np.concatenate([np.ascontiguousarray(b, np.float64).ravel() for b in bases]))
+    out = np.empty((full[mode], rank))
+    _check(lib().ora_compressed_mttkrp(_p(core), _shape(list(core.shape)), _p(flat_b), _shape(full), order,
+                                       _p(_flat(model)), rank, mode, _p(out)))
+    return out
+
+
 def ref_mttkrp(tensor, model, mode):
     t = np.ascontiguousarray(tensor, np.float64)
     shape = list(t.shape)

@@ -15,7 +15,7 @@ from .api import (  # noqa: E402,F401
     InvalidArgument, KruskalModel, LogicError, NcclError, NnlsSolver, ObjectiveProvider, RunTrace, Session,
     SyntheticSpec, TraceRecord, UnsupportedError, ahals_solve, ao_run, default_context, device_count,
     factor_error, generate, her_run, load_tensor, mttkrp_bytes, mttkrp_flops, nnls_solver_from_name, ntft_info,
-    random_init, save_tensor,
+    random_init, save_tensor, TuckerFormat, TuckerProvider, ttm, hosvd_compress, expand,
     slab_range, solve_nnls, stream_seed, update_betas,
 )
 

@@ -94,6 +94,11 @@ SIGNATURES = {
                                                  C.POINTER(C.c_void_p)]),
     "ntf_tensor_upload_rows": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, i64ptr, C.c_int64, C.c_int64,
                                          C.POINTER(C.c_void_p)]),
+    "ntf_tucker_upload": (C.c_int, [C.c_void_p, dptr, C.c_int, i64ptr, dptr, i64ptr, C.POINTER(C.c_void_p)]),
+    "ntf_ntfk_info": (C.c_int, [C.c_char_p, iptr, i64ptr, i64ptr]),
+    "ntf_ntfk_read": (C.c_int, [C.c_char_p, dptr, dptr]),
+    "ntf_ntfk_write": (C.c_int, [C.c_char_p, dptr, dptr, C.c_int, i64ptr, i64ptr]),
+    "ntf_tensor_upload_ntfk": (C.c_int, [C.c_void_p, C.c_char_p, C.POINTER(C.c_void_p)]),
     "ntf_tensor_shape": (C.c_int, [C.c_void_p, iptr, i64ptr]),
     "ntf_tensor_norm_sq": (C.c_int, [C.c_void_p, dptr]),
     "ntf_tensor_destroy": (C.c_int, [C.c_void_p]),

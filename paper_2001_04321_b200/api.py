@@ -574,6 +574,141 @@ class GpuDenseProvider(ObjectiveProvider):
             pass
 
 
+# ---- Tucker-compressed input (include/ntf/tucker.hpp, src/tucker.cpp) ---------------------
+
+@dataclasses.dataclass
+class TuckerFormat:
+    """include/ntf/tucker.hpp:14-35: a core (r_1 x ... x r_N, row-major) and
+    one basis per mode, U_p (I_p x r_p) with orthonormal columns."""
+    core: np.ndarray
+    bases: list
+
+    def full_shape(self):
+        return [int(b.shape[0]) for b in self.bases]
+
+    def ranks(self):
+        return [int(d) for d in np.shape(self.core)]
+
+    def validate(self):
+        """tucker.cpp:16-26 (the GPU upload repeats these checks)."""
+        if len(self.bases) != np.ndim(self.core):
+            raise InvalidArgument("basis count does not match the core order")
+        for p_, b in enumerate(self.bases):
+            if b.shape[1] != np.shape(self.core)[p_]:
+                raise InvalidArgument("basis column count does not match the core shape")
+            if np.max(np.abs(b.T @ b - np.eye(b.shape[1]))) > 1e-10:
+                raise InvalidArgument("basis columns are not orthonormal")
+
+    def _flat(self):
+        core = np.ascontiguousarray(self.core, np.float64)
+        bases = np.ascontiguousarray(np.concatenate([np.ascontiguousarray(b, np.float64).ravel() for b in self.bases]))
+        return core, bases
+
+    def save(self, path):
+        """TuckerFormat::save (tucker.cpp:106-131): the NTFK container."""
+        core, bases = self._flat()
+        full = (C.c_int64 * len(self.bases))(*self.full_shape())
+        ranks = (C.c_int64 * len(self.bases))(*self.ranks())
+        _check(L.lib().ntf_ntfk_write(os.fsencode(path), _dp(core), _dp(bases), len(self.bases), full, ranks))
+
+    @staticmethod
+    def load(path):
+        """TuckerFormat::load (tucker.cpp:133-165)."""
+        order = C.c_int()
+        full = (C.c_int64 * 8)()
+        ranks = (C.c_int64 * 8)()
+        _check(L.lib().ntf_ntfk_info(os.fsencode(path), C.byref(order), full, ranks))
+        n = order.value
+        fs, rs = [int(full[i]) for i in range(n)], [int(ranks[i]) for i in range(n)]
+        core = np.empty(rs)
+        flat = np.empty(sum(a * b for a, b in zip(fs, rs)))
+        _check(L.lib().ntf_ntfk_read(os.fsencode(path), _dp(core), _dp(flat)))
+        bases, off = [], 0
+        for a, b in zip(fs, rs):
+            bases.append(flat[off:off + a * b].reshape(a, b).copy())
+            off += a * b
+        return TuckerFormat(core, bases)
+
+
+def ttm(t, m, mode):
+    """ttm (tucker.cpp:28-33): mode-`mode` product with m (host utility)."""
+    t = np.asarray(t, np.float64)
+    m = np.asarray(m, np.float64)
+    if m.shape[1] != t.shape[mode]:
+        raise InvalidArgument("ttm: dimension mismatch")
+    return np.moveaxis(np.tensordot(m, t, axes=([1], [mode])), 0, mode)
+
+
+def hosvd_compress(t, ranks):
+    """hosvd_compress (tucker.cpp:35-55): per-mode leading left singular
+    vectors of the unfolding (full U, so a rank may exceed the unfolding's
+    column count), core = t contracted with every basis transpose. A host
+    preprocessing utility (numpy LAPACK); the solver path consumes the
+    result through TuckerProvider. Singular vectors are defined up to sign,
+    so the core may differ in sign from Eigen's, the format is equivalent."""
+    t = np.asarray(t, np.float64)
+    n = t.ndim
+    if len(ranks) != n:
+        raise InvalidArgument("hosvd: rank list length does not match the order")
+    for p_ in range(n):
+        if ranks[p_] < 1 or ranks[p_] > t.shape[p_]:
+            raise InvalidArgument("hosvd: rank outside [1, dimension]")
+    bases = []
+    for p_ in range(n):
+        u = np.linalg.svd(np.moveaxis(t, p_, 0).reshape(t.shape[p_], -1), full_matrices=True)[0]
+        bases.append(np.ascontiguousarray(u[:, :ranks[p_]]))
+    core = t
+    for p_ in range(n):
+        core = ttm(core, bases[p_].T, p_)
+    return TuckerFormat(np.ascontiguousarray(core), bases)
+
+
+def expand(fmt: TuckerFormat):
+    """expand (tucker.cpp:57-60): the dense tensor of the format (tests, export)."""
+    t = np.asarray(fmt.core, np.float64)
+    for p_, b in enumerate(fmt.bases):
+        t = ttm(t, b, p_)
+    return np.ascontiguousarray(t)
+
+
+class TuckerProvider(GpuDenseProvider):
+    """TuckerProvider (tucker.hpp:60-73) on the GPU: the MTTKRP runs in the
+    compressed space (ntf_tucker_upload: P_l = U_l^T A_l, the core's MTTKRP
+    on the dense kernels, U_mode times it; tucker.cpp:62-77) and
+    norm_sq() is ||core||^2. The drivers accept it like the dense provider."""
+
+    def __init__(self, fmt: TuckerFormat, ctx: Optional[Context] = None):
+        self.ctx = ctx or default_context()
+        core, bases = fmt._flat()
+        n = len(fmt.bases)
+        if np.ndim(fmt.core) != n:
+            raise InvalidArgument("basis count does not match the core order")
+        h = C.c_void_p()
+        _check(L.lib().ntf_tucker_upload(self.ctx.handle, _dp(core), n, (C.c_int64 * n)(*fmt.ranks()), _dp(bases),
+                                         (C.c_int64 * n)(*fmt.full_shape()), C.byref(h)))
+        self.handle = h
+        self._shape = fmt.full_shape()
+        self.dtype = np.float64
+        self.ranks = fmt.ranks()
+
+    @classmethod
+    def from_ntfk(cls, path, ctx: Optional[Context] = None):
+        """TuckerFormat::load straight into a provider (ntf_tensor_upload_ntfk)."""
+        self = cls.__new__(cls)
+        self.ctx = ctx or default_context()
+        h = C.c_void_p()
+        _check(L.lib().ntf_tensor_upload_ntfk(self.ctx.handle, os.fsencode(path), C.byref(h)))
+        self.handle = h
+        order = C.c_int()
+        full = (C.c_int64 * 8)()
+        ranks = (C.c_int64 * 8)()
+        _check(L.lib().ntf_ntfk_info(os.fsencode(path), C.byref(order), full, ranks))
+        self._shape = [int(full[i]) for i in range(order.value)]
+        self.ranks = [int(ranks[i]) for i in range(order.value)]
+        self.dtype = np.float64
+        return self
+
+
 def solve_nnls(solver, gram, target, init, stop: Optional[InnerStop] = None, ctx: Optional[Context] = None,
                return_sweeps=False):
     """solve_nnls (nnls.cpp:213-222) on the GPU (AHALS only)."""
@@ -618,7 +753,7 @@ def _provider(data, ctx=None):
     if isinstance(data, GpuDenseProvider):
         return data
     if isinstance(data, ObjectiveProvider):
-        raise UnsupportedError("her_run/ao_run need a GPU-resident provider (GpuDenseProvider)")
+        raise UnsupportedError("her_run/ao_run need a GPU-resident provider (GpuDenseProvider, TuckerProvider)")
     return GpuDenseProvider(data, ctx)
 
 

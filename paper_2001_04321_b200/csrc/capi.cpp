@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cmath>
 #include <memory>
 #include <cstring>
 #include <string>
@@ -544,6 +545,117 @@ int ntf_tensor_upload_rows(ntf_ctx* ctx, const void* host, int dtype, int order,
     need(out, "out");
     if (row_begin < 0) throw InvalidArgument("row slab outside the first mode");
     *out = make_tensor(ctx, host, false, dtype, order, shape, (long long)row_begin, (long long)row_end);
+  });
+}
+
+// TuckerFormat::validate (tucker.cpp:16-26) + TuckerProvider (tucker.hpp:60-73)
+ntf_tensor* make_tucker(ntf_ctx* ctx, const double* core, int order, const int64_t* core_shape, const double* bases,
+                        const int64_t* full_shape) {
+  need(ctx, "ctx");
+  need(core, "core");
+  need(core_shape, "core_shape");
+  need(bases, "bases");
+  need(full_shape, "full_shape");
+  if (ctx->comm.active()) throw Unsupported("a Tucker provider lives on one GPU (no NCCL context)");
+  if (order < 1 || order > NTF_MAX_ORDER) throw InvalidArgument("basis count does not match the core order");
+  long long off = 0;
+  for (int l = 0; l < order; ++l) {
+    if (full_shape[l] < 1 || core_shape[l] < 1 || full_shape[l] > (1LL << 31) - 1)
+      throw InvalidArgument("basis column count does not match the core shape");
+    const long long I = full_shape[l], R = core_shape[l];
+    const double* U = bases + off;
+    double defect = 0.0;  // max |U^T U - I|
+    for (long long a = 0; a < R; ++a)
+      for (long long b = 0; b < R; ++b) {
+        double g = 0.0;
+        for (long long i = 0; i < I; ++i) g += U[i * R + a] * U[i * R + b];
+        defect = std::max(defect, std::abs(g - (a == b ? 1.0 : 0.0)));
+      }
+    if (!(defect <= 1e-10)) throw InvalidArgument("basis columns are not orthonormal");
+    off += I * R;
+  }
+  ntf_tensor* c = make_tensor(ctx, core, false, NTF_DTYPE_F64, order, core_shape);
+  auto* t = new ntf_tensor();
+  try {
+    t->core.reset(c);
+    t->ctx = ctx;
+    t->kind = 1;
+    t->dtype = NTF_DTYPE_F64;
+    t->order = order;
+    for (int l = 0; l < order; ++l) {
+      t->shape[l] = full_shape[l];
+      t->ranks[l] = core_shape[l];
+    }
+    t->row0 = 0;
+    t->rows = full_shape[0];
+    t->n_local = 0;
+    t->bases = DevBuf(size_t(off) * sizeof(double));
+    NTF_CUDA(cudaMemcpyAsync(t->bases.p, bases, size_t(off) * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    t->nsq = c->nsq;  // ||core||^2 == ||T||^2 for orthonormal bases (tucker.cpp:94-95)
+    t->nsq_dev = DevBuf(sizeof(double));
+    NTF_CUDA(cudaMemcpyAsync(t->nsq_dev.p, c->nsq_dev.p, sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+    NTF_CUDA(cudaStreamSynchronize(ctx->stream));
+  } catch (...) {
+    delete t;
+    throw;
+  }
+  return t;
+}
+
+int ntf_tucker_upload(ntf_ctx* ctx, const double* core, int order, const int64_t* core_shape, const double* bases,
+                      const int64_t* full_shape, ntf_tensor** out) {
+  return guarded([&] {
+    need(out, "out");
+    *out = make_tucker(ctx, core, order, core_shape, bases, full_shape);
+  });
+}
+
+int ntf_ntfk_info(const char* path, int* order, int64_t* full_shape, int64_t* core_shape) {
+  return guarded([&] {
+    need(path, "path");
+    const NtfkHeader h = ntfk_read_header(path);
+    if (order) *order = h.order;
+    for (int l = 0; l < h.order; ++l) {
+      if (full_shape) full_shape[l] = h.shape[l];
+      if (core_shape) core_shape[l] = h.ranks[l];
+    }
+  });
+}
+
+int ntf_ntfk_read(const char* path, double* core, double* bases) {
+  return guarded([&] {
+    need(path, "path");
+    need(core, "core");
+    need(bases, "bases");
+    ntfk_read(path, core, bases);
+  });
+}
+
+int ntf_ntfk_write(const char* path, const double* core, const double* bases, int order, const int64_t* full_shape,
+                   const int64_t* core_shape) {
+  return guarded([&] {
+    need(path, "path");
+    need(core, "core");
+    need(bases, "bases");
+    need(full_shape, "full_shape");
+    need(core_shape, "core_shape");
+    ntfk_write(path, core, bases, order, full_shape, core_shape);
+  });
+}
+
+int ntf_tensor_upload_ntfk(ntf_ctx* ctx, const char* path, ntf_tensor** out) {
+  return guarded([&] {
+    need(out, "out");
+    need(path, "path");
+    const NtfkHeader h = ntfk_read_header(path);
+    long long nc = 1, nb = 0;
+    for (int l = 0; l < h.order; ++l) {
+      nc *= h.ranks[l];
+      nb += h.shape[l] * h.ranks[l];
+    }
+    std::vector<double> core(static_cast<size_t>(nc)), bases(static_cast<size_t>(nb));
+    ntfk_read(path, core.data(), bases.data());
+    *out = make_tucker(ctx, core.data(), h.order, h.ranks, bases.data(), h.shape);
   });
 }
 

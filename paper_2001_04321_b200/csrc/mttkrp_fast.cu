@@ -9,6 +9,7 @@
 
 #include "mttkrp_fast.h"
 #include "mttkrp_fast_launch.h"
+#include "mttkrp_sk.h"
 
 namespace ntfb {
 
@@ -204,6 +205,8 @@ bool fast_mttkrp_supported(const ModeView& v, int dtype) {
 }
 
 int fast_mttkrp_kernels(const ModeView& v, int dtype) {
+  SkPlan sp;
+  if (sk_choose(v, dtype, device_sm_count(), &sp)) return 1;
   Choice ch;
   if (!choose(v, dtype, device_sm_count(), &ch)) return 2;
   return ch.p.ctas_per_mtile == 1 ? 1 : 2;  // upper bound (2 without an arrival counter)
@@ -212,7 +215,7 @@ int fast_mttkrp_kernels(const ModeView& v, int dtype) {
 size_t fast_mttkrp_partial_len(const ModeView& v, int dtype, int sms) {
   Choice ch;
   if (!choose(v, dtype, sms, &ch)) return 0;
-  return size_t(ch.p.ctas_per_mtile) * v.I * v.rank;
+  return std::max<size_t>(size_t(ch.p.ctas_per_mtile) * size_t(v.I) * size_t(v.rank), sk_partial_len(v, dtype, sms));
 }
 
 namespace {
@@ -301,6 +304,8 @@ std::vector<int> fast_mttkrp_unit_table(const ModeView& v, int dtype, int sms) {
       }
     for (int t = 0; t < m.nb; ++t) e[6 + fast::kMaxBase + t] = dig[m.bq[t]] + (m.bq[t] == 0 ? int(v.row0) : 0);
   }
+  SkPlan sp;  // the stream-K kernel reads its tile tables after the units
+  if (sk_choose(v, dtype, sms, &sp) && sp.layout == ch.layout) sk_append_tables(sp, &tab);
   return tab;
 }
 
@@ -309,6 +314,15 @@ void fast_mttkrp(const void* t, int dtype, const ModeView& v, const DevFactors* 
   Choice ch;
   if (!choose(v, dtype, sms, &ch)) throw Unsupported("no fast MTTKRP plan for this view");
   if (!unit_table) throw LogicError("fast MTTKRP needs its unit table");
+  {
+    SkPlan sp;  // FP64: the persistent stream-K DMMA kernel (mttkrp_sk.cu)
+    if (sk_choose(v, dtype, sms, &sp) && sp.layout == ch.layout) {
+      fast::Params modes{};
+      fill_params_modes(v, sp.layout, modes);
+      sk_mttkrp(t, v, sp, dF, unit_table, partial, out, s, counter, modes);
+      return;
+    }
+  }
   CUtensorMap map;
   make_map(t, dtype, v, ch, &map);
   ch.p.F = dF;
@@ -383,6 +397,8 @@ void fast_mttkrp(const void* t, int dtype, const ModeView& v, const DevFactors* 
 std::string fast_mttkrp_describe(const ModeView& v, int dtype, int sms) {
   Choice ch;
   if (!choose(v, dtype, sms, &ch)) return "generic";
+  SkPlan sp;
+  if (sk_choose(v, dtype, sms, &sp) && sp.layout == ch.layout) return sk_describe(sp);
   char buf[256];
   snprintf(buf, sizeof buf, "%s%s G=%d B=%d A=%d MW=%d KW=%d m_cta=%d stages=%d grid=%d threads=%d smem=%zu units=%lld",
            ch.layout == fast::kRow ? "row" : "col", ch.mma ? "+dmma" : "", ch.cfg.G, ch.cfg.B, ch.cfg.A, ch.p.MW, ch.p.KW, ch.p.m_cta,

@@ -106,6 +106,20 @@ int tree_tiles(const TreeView& v);
 void launch_tree_mttkrp(const double* Y, const TreeView& v, const DevFactors* dF, double* partial, int chunks,
                         unsigned* arrivals, double* out, cudaStream_t s);
 
+// TuckerProvider (tucker.hpp:60-73) on the device: the bases U_l (I_l x r_l,
+// row-major, concatenated) and the projected factors P_l = U_l^T A_l
+// (r_l x r, concatenated) of one MTTKRP (kernels_tucker.cu).
+struct TuckerDev {
+  const double* bases;
+  double* proj;
+  long long base_off[kMaxOrder], proj_off[kMaxOrder];
+  int rows[kMaxOrder], ranks[kMaxOrder];
+};
+// P_l for every l != skip from the X-role factors of dF
+void launch_tucker_project(const TuckerDev& td, const DevFactors* dF, int skip, int order, int rank, cudaStream_t s);
+// out (I_mode x r) = U_mode * Mc (r_mode x r)
+void launch_tucker_expand(const TuckerDev& td, int mode, int rank, const double* Mc, double* out, cudaStream_t s);
+
 // ---- kernel launchers (CUDA translation units) ------------------------------
 struct MttkrpPlan;
 

@@ -181,3 +181,78 @@ void ntft_stream_to_device(const std::string& path, const NtftHeader& h, long lo
 }
 
 }  // namespace ntfb
+
+// ---- "NTFK": TuckerFormat::save / load (tucker.cpp:106-165) -----------------
+// magic "NTFK", u32 version (1), u32 order, u64 full dims, u64 core dims
+// (ranks), the FP64 core payload (last index fastest), then every basis
+// I_p x r_p row-major in mode order. Same messages as TuckerFormat::load.
+namespace ntfb {
+
+namespace {
+constexpr char kMagicK[4] = {'N', 'T', 'F', 'K'};
+}
+
+NtfkHeader ntfk_read_header(const std::string& path) {
+  File in(path, "rb");
+  if (!in.f) throw std::runtime_error("cannot open " + path);
+  char magic[4];
+  if (std::fread(magic, 1, 4, in.f) != 4 || std::memcmp(magic, kMagicK, 4) != 0)
+    throw std::runtime_error(path + ": not a tucker container");
+  uint32_t version = 0, order = 0;
+  if (std::fread(&version, sizeof version, 1, in.f) != 1 || std::fread(&order, sizeof order, 1, in.f) != 1 ||
+      version != kVersion)
+    throw std::runtime_error(path + ": unsupported version");
+  if (order < 1 || order > 64) throw std::runtime_error(path + ": bad order");
+  if (order > uint32_t(kMaxOrder)) throw Unsupported(path + ": order above the GPU path's limit (8)");
+  NtfkHeader h;
+  h.order = int(order);
+  for (int pass = 0; pass < 2; ++pass)
+    for (uint32_t l = 0; l < order; ++l) {
+      uint64_t d = 0;
+      read_exact(in.f, &d, sizeof d, path, "truncated payload");
+      if (d < 1 || d > uint64_t((1LL << 31) - 1)) throw std::runtime_error(path + ": bad dimension");
+      (pass == 0 ? h.shape : h.ranks)[l] = int64_t(d);
+    }
+  h.payload_offset = int64_t(4 + 2 * sizeof(uint32_t) + 2 * order * sizeof(uint64_t));
+  return h;
+}
+
+void ntfk_read(const std::string& path, double* core, double* bases) {
+  const NtfkHeader h = ntfk_read_header(path);
+  long long nc = 1, nb = 0;
+  for (int l = 0; l < h.order; ++l) {
+    nc *= h.ranks[l];
+    nb += h.shape[l] * h.ranks[l];
+  }
+  File in(path, "rb");
+  if (!in.f) throw std::runtime_error("cannot open " + path);
+  if (std::fseek(in.f, long(h.payload_offset), SEEK_SET) != 0) throw std::runtime_error(path + ": truncated payload");
+  read_exact(in.f, core, size_t(nc) * sizeof(double), path, "truncated payload");
+  read_exact(in.f, bases, size_t(nb) * sizeof(double), path, "truncated payload");
+}
+
+void ntfk_write(const std::string& path, const double* core, const double* bases, int order, const int64_t* shape,
+                const int64_t* ranks) {
+  if (order < 1 || order > kMaxOrder) throw InvalidArgument("tensor order must lie in 1..8");
+  long long nc = 1, nb = 0;
+  for (int l = 0; l < order; ++l) {
+    if (shape[l] < 1 || ranks[l] < 1) throw InvalidArgument("tensor dimensions must be positive");
+    nc *= ranks[l];
+    nb += shape[l] * ranks[l];
+  }
+  File out(path, "wb");
+  if (!out.f) throw std::runtime_error("cannot open " + path + " for writing");
+  const uint32_t version = kVersion, ord = uint32_t(order);
+  bool ok = std::fwrite(kMagicK, 1, 4, out.f) == 4 && std::fwrite(&version, sizeof version, 1, out.f) == 1 &&
+            std::fwrite(&ord, sizeof ord, 1, out.f) == 1;
+  for (int pass = 0; pass < 2; ++pass)
+    for (int l = 0; ok && l < order; ++l) {
+      const uint64_t d = uint64_t((pass == 0 ? shape : ranks)[l]);
+      ok = std::fwrite(&d, sizeof d, 1, out.f) == 1;
+    }
+  ok = ok && std::fwrite(core, sizeof(double), size_t(nc), out.f) == size_t(nc);
+  ok = ok && std::fwrite(bases, sizeof(double), size_t(nb), out.f) == size_t(nb);
+  if (!ok || std::fflush(out.f) != 0) throw std::runtime_error("write failed: " + path);
+}
+
+}  // namespace ntfb

@@ -103,6 +103,36 @@ ModeView MttkrpEngine::view(int mode) const {
 
 MttkrpEngine::MttkrpEngine(const ntf_ctx* ctx, const ntf_tensor* t, int rank, unsigned flags)
     : ctx_(ctx), t_(t), rank_(rank), flags_(flags), order_(t->order) {
+  if (t->kind == 1) {  // TuckerProvider: the core's engine plus the projections
+    tucker_ = true;
+    core_eng_ = std::make_unique<MttkrpEngine>(ctx, t->core.get(), rank, flags | NTF_RUN_DIRECT);
+    long long boff = 0, poff = 0, maxr = 1;
+    for (int l = 0; l < t->order; ++l) {
+      td_.rows[l] = int(t->shape[l]);
+      td_.ranks[l] = int(t->ranks[l]);
+      td_.base_off[l] = boff;
+      td_.proj_off[l] = poff;
+      boff += t->shape[l] * t->ranks[l];
+      poff += t->ranks[l] * rank;
+      maxr = std::max(maxr, t->ranks[l]);
+    }
+    proj_ = DevBuf(size_t(poff) * sizeof(double));
+    mc_ = DevBuf(size_t(maxr) * rank * sizeof(double));
+    td_.bases = t->bases.as<double>();
+    td_.proj = proj_.as<double>();
+    std::memset(&core_hF_, 0, sizeof core_hF_);
+    core_hF_.order = t->order;
+    core_hF_.rank = rank;
+    for (int l = 0; l < t->order; ++l) {
+      core_hF_.x[l][0] = core_hF_.x[l][1] = proj_.as<double>() + td_.proj_off[l];
+      core_hF_.rows[l] = td_.ranks[l];
+    }
+    core_dF_ = DevBuf(sizeof(DevFactors));
+    NTF_CUDA(cudaMemcpy(core_dF_.p, &core_hF_, sizeof core_hF_, cudaMemcpyHostToDevice));
+    counter_ = DevBuf(2 * sizeof(unsigned));
+    NTF_CUDA(cudaMemset(counter_.p, 0, 2 * sizeof(unsigned)));
+    return;
+  }
   size_t need = 0;
   for (int m = 0; m < t->order; ++m) {
     const ModeView v = view(m);
@@ -249,6 +279,7 @@ TreeView MttkrpEngine::tree_view(int mode) const {
 }
 
 std::string MttkrpEngine::describe(int mode) const {
+  if (tucker_) return "tucker (project, core " + core_eng_->describe(mode) + ", expand)";
   if (tree_mode(mode))
     return std::string("tree split=") + std::to_string(split_) + " chunks=" + std::to_string(tree_chunks_[mode]) +
            (mode == 0 ? " after Y_L " + fast_mttkrp_describe(ttm_view_, t_->dtype, ctx_->sms) : std::string()) +
@@ -259,6 +290,7 @@ std::string MttkrpEngine::describe(int mode) const {
 }
 
 int MttkrpEngine::kernels_per_call(int mode) const {
+  if (tucker_) return 2 + core_eng_->kernels_per_call(mode);
   // the fast kernel reduces its split-K slabs itself (the engine passes an
   // arrival counter) unless NTF_FAST_SEPARATE_REDUCE asks for the old kernel
   const int fast_kernels = std::getenv("NTF_FAST_SEPARATE_REDUCE") ? 2 : 1;
@@ -273,6 +305,14 @@ int MttkrpEngine::kernels_per_call(int mode) const {
 
 void MttkrpEngine::run(int mode, const DevFactors* dF, double* out, cudaStream_t s, cudaEvent_t ev0,
                        cudaEvent_t ev1) {
+  if (tucker_) {
+    if (ev0) NTF_CUDA(cudaEventRecord(ev0, s));
+    launch_tucker_project(td_, dF, mode, order_, rank_, s);
+    core_eng_->run(mode, core_dF_.as<DevFactors>(), mc_.as<double>(), s);
+    launch_tucker_expand(td_, mode, rank_, mc_.as<double>(), out, s);
+    if (ev1) NTF_CUDA(cudaEventRecord(ev1, s));
+    return;
+  }
   const ModeView v = view(mode);
   const Comm& comm = ctx_->comm;
   const bool gather = comm.active() && mode == 0;
@@ -616,6 +656,8 @@ void Session::kernel_times(double* ms_per_mode, int* launches, int* total_kernel
 }
 
 }  // namespace ntfb
+
+ntf_tensor::~ntf_tensor() = default;
 
 ntf_ctx::~ntf_ctx() {
   if (stream) cudaStreamDestroy(stream);

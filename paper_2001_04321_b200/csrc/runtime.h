@@ -30,6 +30,17 @@ struct NtftHeader {
   int64_t payload_offset = 0;  // bytes
 };
 NtftHeader ntft_read_header(const std::string& path);
+// TuckerFormat container "NTFK" (tucker.cpp:106-165)
+struct NtfkHeader {
+  int order = 0;
+  int64_t shape[kMaxOrder] = {};  // full dims
+  int64_t ranks[kMaxOrder] = {};  // core dims
+  int64_t payload_offset = 0;
+};
+NtfkHeader ntfk_read_header(const std::string& path);
+void ntfk_read(const std::string& path, double* core, double* bases);
+void ntfk_write(const std::string& path, const double* core, const double* bases, int order, const int64_t* shape,
+                const int64_t* ranks);
 void ntft_write(const std::string& path, const void* data, int dtype, int order, const int64_t* shape);
 void ntft_read_slab(const std::string& path, int dtype, int64_t slab_begin, int64_t slab_end, void* out);
 void ntft_stream_to_device(const std::string& path, const NtftHeader& h, long long first, long long count,
@@ -111,6 +122,13 @@ class MttkrpEngine {
   int tree_tiles_max_ = 1;
   DevBuf tree_arrivals_;         // per-tile arrival counters of the tree kernel (self-resetting)
   TreeView tree_view(int mode) const;
+  // TuckerProvider (t->kind == kTucker): P_l = U_l^T A_l, the core's MTTKRP
+  // with P on the dense kernels, then U_mode times it (tucker.cpp:62-77)
+  bool tucker_ = false;
+  std::unique_ptr<MttkrpEngine> core_eng_;
+  TuckerDev td_{};
+  DevFactors core_hF_{};
+  DevBuf proj_, core_dF_, mc_;
 };
 
 // Per-tensor workspace of the per-call provider entry points (ntf_mttkrp,
@@ -194,4 +212,12 @@ struct ntf_tensor {
   double nsq = 0.0;
   bool rows_only = false;  // a caller-chosen row slab on a 1-GPU context (ntf_tensor_upload_rows)
   mutable std::unique_ptr<ntfb::CallCache> cache;
+  // TuckerProvider (kind == 1): the core as a dense device tensor, the bases
+  // (I_l x r_l row-major, concatenated); nsq = ||core||^2 (provider ctor,
+  // tucker.cpp:94-95). `data` is empty: the full tensor never exists.
+  int kind = 0;
+  std::unique_ptr<ntf_tensor> core;
+  ntfb::DevBuf bases;
+  long long ranks[NTF_MAX_ORDER] = {};
+  ~ntf_tensor();
 };
