@@ -11,6 +11,7 @@
 // col-major factors convert with a transpose copy.
 #pragma once
 
+#include <algorithm>
 #include <cstdint>
 #include <functional>
 #include <optional>
@@ -83,7 +84,7 @@ struct AoConfig {
   double max_time_s = 0.0;
   bool record_factor_error = false;
   const KruskalModel* ground_truth = nullptr;
-  unsigned flags = 0;  // NTF_RUN_*
+  unsigned flags = 0;  // NTF_RUN_* (0: dimension tree, graph replay -- the production path)
   void validate() const {
     const ntf_ao_config c = c_struct(nullptr);
     check(ntf_ao_config_validate(&c));
@@ -166,21 +167,13 @@ class ObjectiveProvider {
   virtual Matrix mttkrp(const KruskalModel& m, int mode) const = 0;
 };
 
-// DenseProvider (provider.hpp:22-34) with the tensor resident on the GPU.
-class GpuDenseProvider final : public ObjectiveProvider {
+// A provider whose data lives on the GPU (dense tensor or Tucker format):
+// the drivers below run the whole iteration on the device for any of them.
+class GpuProvider : public ObjectiveProvider {
  public:
-  // `data`: this rank's mode-1 slab (row-major, last index fastest) of a
-  // tensor of full shape `shape`; FP64 or FP32.
-  template <typename T>
-  GpuDenseProvider(Context& ctx, const T* data, const std::vector<int>& shape) : ctx_(&ctx), shape_(shape) {
-    static_assert(std::is_same<T, double>::value || std::is_same<T, float>::value, "FP64 or FP32 tensors");
-    std::vector<int64_t> s(shape.begin(), shape.end());
-    check(ntf_tensor_upload(ctx.get(), data, std::is_same<T, float>::value ? NTF_DTYPE_F32 : NTF_DTYPE_F64,
-                            int(shape.size()), s.data(), &t_));
-  }
-  ~GpuDenseProvider() override { ntf_tensor_destroy(t_); }
-  GpuDenseProvider(const GpuDenseProvider&) = delete;
-  GpuDenseProvider& operator=(const GpuDenseProvider&) = delete;
+  ~GpuProvider() override { ntf_tensor_destroy(t_); }
+  GpuProvider(const GpuProvider&) = delete;
+  GpuProvider& operator=(const GpuProvider&) = delete;
 
   std::vector<int> shape() const override { return shape_; }
   double norm_sq() const override {
@@ -198,10 +191,85 @@ class GpuDenseProvider final : public ObjectiveProvider {
   ntf_ctx* ctx() const { return ctx_->get(); }
   const ntf_tensor* tensor() const { return t_; }
 
- private:
+ protected:
+  GpuProvider(Context& ctx, std::vector<int> shape) : ctx_(&ctx), shape_(std::move(shape)) {}
   Context* ctx_;
   std::vector<int> shape_;
   ntf_tensor* t_ = nullptr;
+};
+
+// DenseProvider (provider.hpp:22-34) with the tensor resident on the GPU.
+class GpuDenseProvider final : public GpuProvider {
+ public:
+  // `data`: this rank's mode-1 slab (row-major, last index fastest) of a
+  // tensor of full shape `shape`; FP64 or FP32.
+  template <typename T>
+  GpuDenseProvider(Context& ctx, const T* data, const std::vector<int>& shape) : GpuProvider(ctx, shape) {
+    static_assert(std::is_same<T, double>::value || std::is_same<T, float>::value, "FP64 or FP32 tensors");
+    std::vector<int64_t> s(shape.begin(), shape.end());
+    check(ntf_tensor_upload(ctx.get(), data, std::is_same<T, float>::value ? NTF_DTYPE_F32 : NTF_DTYPE_F64,
+                            int(shape.size()), s.data(), &t_));
+  }
+};
+
+// TuckerFormat (tucker.hpp:14-35): core (row-major, dims = basis column
+// counts) and one basis per mode with orthonormal columns.
+struct TuckerFormat {
+  std::vector<int> core_shape;
+  std::vector<double> core;
+  std::vector<Matrix> bases;  // I_p x r_p, row-major
+  std::vector<int> full_shape() const {
+    std::vector<int> s;
+    for (const auto& b : bases) s.push_back(int(b.rows));
+    return s;
+  }
+  // TuckerFormat::save / load (tucker.cpp:106-165): the NTFK container
+  void save(const std::string& path) const {
+    std::vector<int64_t> f, r;
+    for (const auto& b : bases) f.push_back(b.rows);
+    for (int d : core_shape) r.push_back(d);
+    const auto flat = flat_bases();
+    check(ntf_ntfk_write(path.c_str(), core.data(), flat.data(), int(bases.size()), f.data(), r.data()));
+  }
+  static TuckerFormat load(const std::string& path) {
+    int order = 0;
+    int64_t f[NTF_MAX_ORDER], r[NTF_MAX_ORDER];
+    check(ntf_ntfk_info(path.c_str(), &order, f, r));
+    TuckerFormat t;
+    int64_t nc = 1, nb = 0;
+    for (int l = 0; l < order; ++l) {
+      t.core_shape.push_back(int(r[l]));
+      nc *= r[l];
+      nb += f[l] * r[l];
+    }
+    t.core.resize(size_t(nc));
+    std::vector<double> flat(static_cast<size_t>(nb));
+    check(ntf_ntfk_read(path.c_str(), t.core.data(), flat.data()));
+    size_t off = 0;
+    for (int l = 0; l < order; ++l) {
+      Matrix b(f[l], r[l]);
+      std::copy(flat.begin() + std::ptrdiff_t(off), flat.begin() + std::ptrdiff_t(off + b.v.size()), b.v.begin());
+      off += b.v.size();
+      t.bases.push_back(std::move(b));
+    }
+    return t;
+  }
+  std::vector<double> flat_bases() const {
+    std::vector<double> flat;
+    for (const auto& b : bases) flat.insert(flat.end(), b.v.begin(), b.v.end());
+    return flat;
+  }
+};
+
+// TuckerProvider (tucker.hpp:60-73): the MTTKRP runs in the compressed space
+// on the GPU; norm_sq() is ||core||^2. Validates like TuckerFormat::validate.
+class TuckerProvider final : public GpuProvider {
+ public:
+  TuckerProvider(Context& ctx, const TuckerFormat& fmt) : GpuProvider(ctx, fmt.full_shape()) {
+    std::vector<int64_t> f(shape_.begin(), shape_.end()), r(fmt.core_shape.begin(), fmt.core_shape.end());
+    const auto flat = fmt.flat_bases();
+    check(ntf_tucker_upload(ctx.get(), fmt.core.data(), int(fmt.bases.size()), r.data(), flat.data(), f.data(), &t_));
+  }
 };
 
 namespace detail {
@@ -221,9 +289,9 @@ inline RunTrace to_trace(double f0, const std::vector<ntf_trace_record>& recs, i
   }
   return t;
 }
-inline const GpuDenseProvider& gpu(const ObjectiveProvider& p) {
-  auto* g = dynamic_cast<const GpuDenseProvider*>(&p);
-  if (!g) throw std::runtime_error("her_run/ao_run need a GPU-resident provider (GpuDenseProvider)");
+inline const GpuProvider& gpu(const ObjectiveProvider& p) {
+  auto* g = dynamic_cast<const GpuProvider*>(&p);
+  if (!g) throw std::runtime_error("her_run/ao_run need a GPU-resident provider (GpuDenseProvider, TuckerProvider)");
   return *g;
 }
 }  // namespace detail

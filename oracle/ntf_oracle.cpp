@@ -342,6 +342,325 @@ Mat ahals_solve(const Mat& g, const Mat& c, const Mat& w0, const InnerStop& stop
   return w;
 }
 
+// ------------------------------------------------ the other inner solvers --
+// Restated from nnls.cpp:51-211 (and spectral_norm, kernels.cpp:262-280),
+// plain ascending loops instead of Eigen: agreement "to rounding".
+
+namespace {
+
+Mat matmul(const Mat& a, const Mat& b) {  // a (n x k) * b (k x m)
+  Mat out(a.rows, b.cols);
+  for (int64_t i = 0; i < a.rows; ++i)
+    for (int64_t j = 0; j < b.cols; ++j) {
+      double acc = 0.0;
+      for (int64_t k = 0; k < a.cols; ++k) acc += a(i, k) * b(k, j);
+      out(i, j) = acc;
+    }
+  return out;
+}
+
+double fro_diff(const Mat& a, const Mat& b) {
+  double sq = 0.0;
+  for (size_t e = 0; e < a.v.size(); ++e) sq += (a.v[e] - b.v[e]) * (a.v[e] - b.v[e]);
+  return std::sqrt(sq);
+}
+
+// Cholesky L L^T = a (lower, row-major); false unless positive definite
+// (Eigen::LLT's info() != Success).
+bool cholesky(const Mat& a, Mat* l) {
+  const int64_t n = a.rows;
+  *l = Mat(n, n);
+  for (int64_t j = 0; j < n; ++j) {
+    double d = a(j, j);
+    for (int64_t k = 0; k < j; ++k) d -= (*l)(j, k) * (*l)(j, k);
+    if (!(d > 0.0)) return false;
+    (*l)(j, j) = std::sqrt(d);
+    for (int64_t i = j + 1; i < n; ++i) {
+      double v = a(i, j);
+      for (int64_t k = 0; k < j; ++k) v -= (*l)(i, k) * (*l)(j, k);
+      (*l)(i, j) = v / (*l)(j, j);
+    }
+  }
+  return true;
+}
+
+// x = (L L^T)^{-1} b for one vector
+std::vector<double> chol_solve(const Mat& l, std::vector<double> b) {
+  const int64_t n = l.rows;
+  for (int64_t i = 0; i < n; ++i) {
+    for (int64_t k = 0; k < i; ++k) b[size_t(i)] -= l(i, k) * b[size_t(k)];
+    b[size_t(i)] /= l(i, i);
+  }
+  for (int64_t i = n - 1; i >= 0; --i) {
+    for (int64_t k = i + 1; k < n; ++k) b[size_t(i)] -= l(k, i) * b[size_t(k)];
+    b[size_t(i)] /= l(i, i);
+  }
+  return b;
+}
+
+// Largest |eigenvalue| of a symmetric matrix by cyclic Jacobi rotations:
+// the fallback of spectral_norm (Eigen::SelfAdjointEigenSolver there).
+double jacobi_max_abs_eig(Mat a) {
+  const int64_t n = a.rows;
+  for (int sweep = 0; sweep < 100; ++sweep) {
+    double off = 0.0;
+    for (int64_t p = 0; p < n; ++p)
+      for (int64_t q = p + 1; q < n; ++q) off += a(p, q) * a(p, q);
+    if (off <= 1e-300) break;
+    for (int64_t p = 0; p < n; ++p)
+      for (int64_t q = p + 1; q < n; ++q) {
+        if (a(p, q) == 0.0) continue;
+        const double theta = (a(q, q) - a(p, p)) / (2.0 * a(p, q));
+        const double t = (theta >= 0 ? 1.0 : -1.0) / (std::abs(theta) + std::sqrt(theta * theta + 1.0));
+        const double c = 1.0 / std::sqrt(t * t + 1.0), s = t * c;
+        for (int64_t k = 0; k < n; ++k) {
+          const double akp = a(k, p), akq = a(k, q);
+          a(k, p) = c * akp - s * akq;
+          a(k, q) = s * akp + c * akq;
+        }
+        for (int64_t k = 0; k < n; ++k) {
+          const double apk = a(p, k), aqk = a(q, k);
+          a(p, k) = c * apk - s * aqk;
+          a(q, k) = s * apk + c * aqk;
+        }
+      }
+  }
+  double m = 0.0;
+  for (int64_t i = 0; i < n; ++i) m = std::max(m, std::abs(a(i, i)));
+  return m;
+}
+
+}  // namespace
+
+// kernels.cpp:262-280: power iteration from the normalised ones vector.
+double spectral_norm(const Mat& m) {
+  const int64_t r = m.rows;
+  if (r == 0) return 0.0;
+  if (r == 1) return std::abs(m(0, 0));
+  std::vector<double> v(static_cast<size_t>(r), 1.0 / std::sqrt(double(r))), w(static_cast<size_t>(r));
+  double lambda = 0.0;
+  for (int it = 0; it < 1000; ++it) {
+    double nrm = 0.0;
+    for (int64_t i = 0; i < r; ++i) {
+      double acc = 0.0;
+      for (int64_t k = 0; k < r; ++k) acc += m(i, k) * v[size_t(k)];
+      w[size_t(i)] = acc;
+      nrm += acc * acc;
+    }
+    nrm = std::sqrt(nrm);
+    if (nrm == 0.0) return 0.0;
+    for (int64_t i = 0; i < r; ++i) v[size_t(i)] = w[size_t(i)] / nrm;
+    double next = 0.0;
+    for (int64_t i = 0; i < r; ++i) {
+      double acc = 0.0;
+      for (int64_t k = 0; k < r; ++k) acc += m(i, k) * v[size_t(k)];
+      next += v[size_t(i)] * acc;
+    }
+    if (std::abs(next - lambda) <= 1e-10 * std::max(1.0, std::abs(next))) return next;
+    lambda = next;
+  }
+  return jacobi_max_abs_eig(m);
+}
+
+// nnls.cpp:11-13: 0.5 <W^T W, G> - <W, C>.
+double nnls_objective(const Mat& g, const Mat& c, const Mat& w) {
+  const Mat ww = gram(w);
+  double q = 0.0, l = 0.0;
+  for (size_t e = 0; e < ww.v.size(); ++e) q += ww.v[e] * g.v[e];
+  for (size_t e = 0; e < w.v.size(); ++e) l += w.v[e] * c.v[e];
+  return 0.5 * q - l;
+}
+
+// nnls.cpp:51-57 (run_sweeps, nnls.cpp:31-44: stop on the first change).
+Mat pgd_solve(const Mat& g, const Mat& c, const Mat& w0, const InnerStop& stop) {
+  const double lip = spectral_norm(g);
+  if (lip <= 0.0) throw std::runtime_error("pgd_solve: zero Gram matrix");
+  Mat w = w0;
+  double first = -1.0;
+  for (int s = 0; s < stop.max_iters; ++s) {
+    const Mat wg = matmul(w, g);
+    Mat next(w.rows, w.cols);
+    for (size_t e = 0; e < w.v.size(); ++e) next.v[e] = std::max(0.0, w.v[e] - (wg.v[e] - c.v[e]) / lip);
+    const double change = fro_diff(next, w);
+    w = std::move(next);
+    if (s == 0) first = change;
+    if (change <= stop.rel_change_tol * first) break;
+  }
+  return w;
+}
+
+// nnls.cpp:59-87.
+Mat nesterov_solve(const Mat& g, const Mat& c, const Mat& w0, const InnerStop& stop) {
+  const double lip = spectral_norm(g);
+  if (lip <= 0.0) throw std::runtime_error("nesterov_solve: zero Gram matrix");
+  Mat w = w0, y = w0, best = w0;
+  double best_obj = nnls_objective(g, c, w);
+  double t = 1.0, first = -1.0;
+  for (int s = 0; s < stop.max_iters; ++s) {
+    const Mat yg = matmul(y, g);
+    Mat next(w.rows, w.cols);
+    for (size_t e = 0; e < w.v.size(); ++e) next.v[e] = std::max(0.0, y.v[e] - (yg.v[e] - c.v[e]) / lip);
+    const double t_next = 0.5 * (1.0 + std::sqrt(1.0 + 4.0 * t * t));
+    for (size_t e = 0; e < w.v.size(); ++e) y.v[e] = next.v[e] + ((t - 1.0) / t_next) * (next.v[e] - w.v[e]);
+    const double change = fro_diff(next, w);
+    w = std::move(next);
+    t = t_next;
+    const double obj = nnls_objective(g, c, w);
+    if (obj < best_obj) {
+      best_obj = obj;
+      best = w;
+    }
+    if (s == 0) first = change;
+    if (change <= stop.rel_change_tol * first) break;
+  }
+  return best;
+}
+
+// nnls.cpp:89-121.
+Mat admm_solve(const Mat& g, const Mat& c, const Mat& w0, const InnerStop& stop) {
+  const int64_t r = g.rows;
+  double tr = 0.0;
+  for (int64_t j = 0; j < r; ++j) tr += g(j, j);
+  const double rho = tr / double(r);
+  if (rho <= 0.0) throw std::runtime_error("admm_solve: zero Gram matrix");
+  Mat shifted = g;
+  for (int64_t j = 0; j < r; ++j) shifted(j, j) += rho;
+  Mat l;
+  if (!cholesky(shifted, &l)) throw std::runtime_error("admm_solve: factorization failed");
+  Mat z = w0, u(w0.rows, w0.cols), best = w0;
+  double best_obj = nnls_objective(g, c, z);
+  double first = -1.0;
+  for (int s = 0; s < stop.max_iters; ++s) {
+    Mat w(z.rows, z.cols), zn(z.rows, z.cols);
+    for (int64_t i = 0; i < z.rows; ++i) {  // W (G + rho I) = C + rho (Z - U), row by row
+      std::vector<double> rhs(static_cast<size_t>(r));
+      for (int64_t j = 0; j < r; ++j) rhs[size_t(j)] = c(i, j) + rho * (z(i, j) - u(i, j));
+      const std::vector<double> x = chol_solve(l, rhs);
+      for (int64_t j = 0; j < r; ++j) w(i, j) = x[size_t(j)];
+    }
+    for (size_t e = 0; e < z.v.size(); ++e) {
+      zn.v[e] = std::max(0.0, w.v[e] + u.v[e]);
+      u.v[e] += w.v[e] - zn.v[e];
+    }
+    const double change = fro_diff(zn, z);
+    z = std::move(zn);
+    const double obj = nnls_objective(g, c, z);
+    if (obj < best_obj) {
+      best_obj = obj;
+      best = z;
+    }
+    if (s == 0) first = change;
+    if (change <= stop.rel_change_tol * first) break;
+  }
+  return best;
+}
+
+namespace {
+
+// nnls.cpp:125-191: Lawson-Hanson on the normal equations for one row.
+bool solve_row_active_set(const Mat& g, const std::vector<double>& c, std::vector<double>& x) {
+  const int64_t r = g.rows;
+  double cmax = 0.0, gmax = -std::numeric_limits<double>::infinity();
+  for (int64_t j = 0; j < r; ++j) {
+    cmax = std::max(cmax, std::abs(c[size_t(j)]));
+    gmax = std::max(gmax, g(j, j));
+  }
+  const double enter_tol = 1e-11 * std::max({1.0, cmax, gmax});
+  x.assign(size_t(r), 0.0);
+  std::vector<int64_t> passive;
+  std::vector<bool> in_passive(size_t(r), false);
+  const int max_additions = 3 * int(r);
+  for (int additions = 0;; ++additions) {
+    int64_t enter = -1;
+    double best = enter_tol;
+    for (int64_t j = 0; j < r; ++j) {
+      double gx = 0.0;
+      for (int64_t k = 0; k < r; ++k) gx += g(j, k) * x[size_t(k)];
+      const double dual = c[size_t(j)] - gx;
+      if (!in_passive[size_t(j)] && dual > best) {
+        best = dual;
+        enter = j;
+      }
+    }
+    if (enter < 0) return true;
+    if (additions >= max_additions) return false;
+    passive.push_back(enter);
+    in_passive[size_t(enter)] = true;
+    for (;;) {
+      const int64_t np = int64_t(passive.size());
+      Mat gp(np, np);
+      std::vector<double> cp(static_cast<size_t>(np));
+      for (int64_t a = 0; a < np; ++a) {
+        cp[size_t(a)] = c[size_t(passive[size_t(a)])];
+        for (int64_t b = 0; b < np; ++b) gp(a, b) = g(passive[size_t(a)], passive[size_t(b)]);
+      }
+      Mat l;
+      cholesky(gp, &l);  // Eigen's llt().solve on a positive-definite principal submatrix
+      const std::vector<double> zp = chol_solve(l, cp);
+      bool all_pos = true;
+      for (double v : zp) all_pos = all_pos && v > 0.0;
+      if (all_pos) {
+        std::fill(x.begin(), x.end(), 0.0);
+        for (int64_t a = 0; a < np; ++a) x[size_t(passive[size_t(a)])] = zp[size_t(a)];
+        break;
+      }
+      double alpha = 1.0;
+      for (int64_t a = 0; a < np; ++a)
+        if (zp[size_t(a)] <= 0.0) {
+          const double xa = x[size_t(passive[size_t(a)])];
+          alpha = std::min(alpha, xa / (xa - zp[size_t(a)]));
+        }
+      for (int64_t a = 0; a < np; ++a) {
+        const int64_t j = passive[size_t(a)];
+        x[size_t(j)] += alpha * (zp[size_t(a)] - x[size_t(j)]);
+      }
+      for (size_t a = passive.size(); a-- > 0;) {
+        const int64_t j = passive[a];
+        if (x[size_t(j)] <= 0.0 || (zp[a] <= 0.0 && x[size_t(j)] < 1e-14)) {
+          x[size_t(j)] = 0.0;
+          in_passive[size_t(j)] = false;
+          passive.erase(passive.begin() + std::ptrdiff_t(a));
+        }
+      }
+    }
+  }
+}
+
+}  // namespace
+
+// nnls.cpp:195-211.
+Mat active_set_solve(const Mat& g, const Mat& c) {
+  Mat l;
+  if (!cholesky(g, &l)) throw std::runtime_error("active_set_solve: Gram matrix is not positive definite");
+  Mat w(c.rows, g.cols);
+  bool ok = true;
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < c.rows; ++i) {
+    std::vector<double> row(static_cast<size_t>(c.cols)), x;
+    for (int64_t j = 0; j < c.cols; ++j) row[size_t(j)] = c(i, j);
+    if (solve_row_active_set(g, row, x)) {
+      for (int64_t j = 0; j < c.cols; ++j) w(i, j) = x[size_t(j)];
+    } else {
+#pragma omp atomic write
+      ok = false;
+    }
+  }
+  if (!ok) throw std::runtime_error("active_set_solve: pass budget exceeded");
+  return w;
+}
+
+// nnls.cpp:213-222.
+Mat solve_nnls(int solver, const Mat& g, const Mat& c, const Mat& w0, const InnerStop& stop) {
+  switch (solver) {
+    case kAhals: return ahals_solve(g, c, w0, stop, nullptr);
+    case kAdmm: return admm_solve(g, c, w0, stop);
+    case kNesterov: return nesterov_solve(g, c, w0, stop);
+    case kPgd: return pgd_solve(g, c, w0, stop);
+    case kActiveSet: return active_set_solve(g, c);
+  }
+  throw std::logic_error("unknown solver");
+}
+
 // ---------------------------------------------------------------- drivers --
 
 // src/her.cpp:10-14.
@@ -449,7 +768,7 @@ Model her_run(const T* data, const std::vector<int>& shape, const Model& init, c
     for (int i = 0; i < n; ++i) {
       const Mat g = hadamard_of_grams(hat_grams, i);
       Mat c = mttkrp(data, shape, hat, i);
-      solved[size_t(i)] = ahals_solve(g, c, accepted[size_t(i)], cfg.inner, nullptr);
+      solved[size_t(i)] = solve_nnls(cfg.solver, g, c, accepted[size_t(i)], cfg.inner);
       hat[size_t(i)] = extrapolate_block(solved[size_t(i)], accepted[size_t(i)], beta_used);
       hat_grams[size_t(i)] = gram(hat[size_t(i)]);
       if (i == n - 1) last_c = std::move(c);
@@ -511,7 +830,7 @@ Model ao_run(const T* data, const std::vector<int>& shape, const Model& init, co
     for (int i = 0; i < n; ++i) {
       const Mat g = hadamard_of_grams(grams, i);
       const Mat c = mttkrp(data, shape, model, i);
-      Mat w = ahals_solve(g, c, model[size_t(i)], cfg.inner, nullptr);
+      Mat w = solve_nnls(cfg.solver, g, c, model[size_t(i)], cfg.inner);
       if (i == n - 1) f = cheap_objective(nsq, w, g, c);
       model[size_t(i)] = std::move(w);
       grams[size_t(i)] = gram(model[size_t(i)]);

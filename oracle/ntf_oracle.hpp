@@ -81,7 +81,18 @@ Mat hals_pass(const Mat& g, const Mat& c, Mat w);
 Mat ahals_solve(const Mat& g, const Mat& c, const Mat& w0, const InnerStop& stop, int* sweeps_out);
 
 // ---- drivers (ao.cpp, her.cpp, driver_common.hpp) --------------------------
+// NnlsSolver (nnls.hpp:53) and the solvers of nnls.cpp:51-211.
+enum Solver { kAhals = 0, kAdmm = 1, kNesterov = 2, kPgd = 3, kActiveSet = 4 };
+double spectral_norm(const Mat& m);
+double nnls_objective(const Mat& g, const Mat& c, const Mat& w);
+Mat pgd_solve(const Mat& g, const Mat& c, const Mat& w0, const InnerStop& stop);
+Mat nesterov_solve(const Mat& g, const Mat& c, const Mat& w0, const InnerStop& stop);
+Mat admm_solve(const Mat& g, const Mat& c, const Mat& w0, const InnerStop& stop);
+Mat active_set_solve(const Mat& g, const Mat& c);
+Mat solve_nnls(int solver, const Mat& g, const Mat& c, const Mat& w0, const InnerStop& stop);
+
 struct AoConfig {
+  int solver = kAhals;
   InnerStop inner;
   int max_outer_iters = 0;
   double max_time_s = 0.0;

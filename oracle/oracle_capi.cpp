@@ -230,7 +230,7 @@ void obs_tramp(void* u, int k, double f, int rs, double b, const ora::Model& acc
 }  // namespace
 
 // algo: 0 = HER, 1 = AO. truth may be null (no e_k).
-int ora_run(int algo, const void* tensor, int dtype, const int* shape, int order, const double* init,
+int ora_run(int algo, int solver, const void* tensor, int dtype, const int* shape, int order, const double* init,
             int rank, int inner_max_iters, double inner_tol, int max_outer_iters, double max_time_s,
             const double* truth, double beta0, double gamma, double gamma_bar, double eta,
             double* out_factors, double* f0, void* records, int cap, int* n_records,
@@ -241,6 +241,7 @@ int ora_run(int algo, const void* tensor, int dtype, const int* shape, int order
     ora::Model tm;
     ora::AoConfig cfg;
     cfg.inner = ora::InnerStop{inner_max_iters, inner_tol};
+    cfg.solver = solver;
     cfg.max_outer_iters = max_outer_iters;
     cfg.max_time_s = max_time_s;
     if (truth) {
@@ -309,4 +310,23 @@ extern "C" int ora_compressed_mttkrp(const double* core, const int* core_shape, 
     g_err = e.what();
     return 2;
   }
+}
+
+// solve_nnls (nnls.cpp:213-222) with any solver: g r x r, c / w0 / out rows x r.
+extern "C" int ora_solve_nnls(int solver, const double* g, const double* c, const double* w0, int rows, int r,
+                              int max_iters, double tol, double* out) {
+  return guard([&] {
+    ora::Mat gm(r, r), cm(rows, r), wm(rows, r);
+    std::memcpy(gm.v.data(), g, gm.v.size() * sizeof(double));
+    std::memcpy(cm.v.data(), c, cm.v.size() * sizeof(double));
+    std::memcpy(wm.v.data(), w0, wm.v.size() * sizeof(double));
+    const ora::Mat w = ora::solve_nnls(solver, gm, cm, wm, ora::InnerStop{max_iters, tol});
+    std::memcpy(out, w.v.data(), w.v.size() * sizeof(double));
+  });
+}
+
+extern "C" double ora_spectral_norm(const double* g, int r) {
+  ora::Mat gm(r, r);
+  std::memcpy(gm.v.data(), g, gm.v.size() * sizeof(double));
+  return ora::spectral_norm(gm);
 }

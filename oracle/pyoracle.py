@@ -270,8 +270,28 @@ def hungarian(cost):
     return list(mapping), total.value
 
 
+SOLVERS = {"ahals": 0, "admm": 1, "nesterov": 2, "pgd": 3, "active_set": 4, "as": 4}
+
+
+def solve_nnls(solver, g, c, w0, max_iters=50, tol=1e-2):
+    """solve_nnls (nnls.cpp:213-222) with any solver name."""
+    g, c, w0 = (np.ascontiguousarray(x, np.float64) for x in (g, c, w0))
+    out = np.empty_like(w0)
+    _check(lib().ora_solve_nnls(SOLVERS[solver], _p(g), _p(c), _p(w0), w0.shape[0], w0.shape[1], max_iters,
+                                C.c_double(tol), _p(out)))
+    return out
+
+
+def spectral_norm(g):
+    """kernels.cpp:262-280."""
+    g = np.ascontiguousarray(g, np.float64)
+    L = lib()
+    L.ora_spectral_norm.restype = C.c_double
+    return L.ora_spectral_norm(_p(g), g.shape[0])
+
+
 def run(algo, tensor, init, max_outer_iters=0, max_time_s=0.0, inner_max_iters=50, inner_tol=1e-2,
-        truth=None, beta0=0.5, gamma=1.05, gamma_bar=1.01, eta=1.5, observer=None):
+        truth=None, beta0=0.5, gamma=1.05, gamma_bar=1.01, eta=1.5, observer=None, solver="ahals"):
     """Oracle her_run (algo='her') / ao_run (algo='ao').
 
     Returns (factors, f0, records) with records a list of dicts in the
@@ -294,7 +314,7 @@ def run(algo, tensor, init, max_outer_iters=0, max_time_s=0.0, inner_max_iters=5
         cb = OBSERVER(_tramp)
     L = lib()
     truth_ptr = _p(_flat(truth)) if truth is not None else C.cast(None, _dptr)
-    _check(L.ora_run(0 if algo == "her" else 1, t.ctypes.data_as(C.c_void_p), _dtype_code(t),
+    _check(L.ora_run(0 if algo == "her" else 1, SOLVERS[solver], t.ctypes.data_as(C.c_void_p), _dtype_code(t),
                      _shape(shape), len(shape), _p(_flat(init)), rank, inner_max_iters, C.c_double(inner_tol),
                      max_outer_iters, C.c_double(max_time_s), truth_ptr, C.c_double(beta0), C.c_double(gamma),
                      C.c_double(gamma_bar), C.c_double(eta), _p(out), C.byref(f0), recs, cap, C.byref(n),

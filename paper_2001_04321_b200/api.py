@@ -72,7 +72,8 @@ def _dp(a):
 # ---- configuration (nnls.hpp, ao.hpp, her.hpp) ----------------------------------
 
 class NnlsSolver(enum.IntEnum):
-    """include/ntf/nnls.hpp:53. Only ``ahals`` runs on the GPU path."""
+    """include/ntf/nnls.hpp:53. All run on the GPU: ``ahals`` in the fused
+    block-update kernel, the others in kernels_solvers.cu (nnls.cpp:51-211)."""
     ahals = 0
     admm = 1
     nesterov = 2
@@ -711,7 +712,8 @@ class TuckerProvider(GpuDenseProvider):
 
 def solve_nnls(solver, gram, target, init, stop: Optional[InnerStop] = None, ctx: Optional[Context] = None,
                return_sweeps=False):
-    """solve_nnls (nnls.cpp:213-222) on the GPU (AHALS only)."""
+    """solve_nnls (nnls.cpp:213-222) on the GPU, every solver. ``return_sweeps``
+    reports the sweeps run (AHALS, PGD, Nesterov, ADMM; 0 for the active set)."""
     ctx = ctx or default_context()
     g = np.ascontiguousarray(gram, np.float64)
     c = np.ascontiguousarray(target, np.float64)

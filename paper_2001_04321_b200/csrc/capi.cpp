@@ -91,8 +91,9 @@ void check_run_inputs(const ntf_tensor* t, const double* init, int rank, const n
   const long long n = model_len(t, rank);
   for (long long e = 0; e < n; ++e)
     if (init[e] < 0.0) throw InvalidArgument("initial model must be entrywise nonnegative");
-  if (cfg.solver != NTF_SOLVER_AHALS)
-    throw Unsupported("only the AHALS inner solver runs on the GPU path");
+  if (cfg.solver < NTF_SOLVER_AHALS || cfg.solver > NTF_SOLVER_ACTIVE_SET) throw LogicError("unknown solver");
+  if (cfg.solver == NTF_SOLVER_ACTIVE_SET && rank > 32)
+    throw Unsupported("the GPU active-set solver serves ranks up to 32");
   if (cfg.inner_stop.max_iters < 0) throw InvalidArgument("inner max_iters must be >= 0");
   // the fused block update keeps a factor on one thread-block cluster
   // (launch_nnls): refuse up front, before the session is built
@@ -269,6 +270,7 @@ void run_driver(int algo, ntf_ctx* ctx, const ntf_tensor* t, const double* init,
       if (finished) break;
     }
   }
+  s.check_error();
   s.factors(out_factors);
   std::vector<ntf_trace_record> recs(size_t(std::max(trace_cap, 0)));
   int n = 0;
@@ -759,7 +761,7 @@ int ntf_solve_nnls(ntf_ctx* ctx, int solver, const double* gram, const double* t
     need(target, "target");
     need(init, "init");
     need(out, "out");
-    if (solver != NTF_SOLVER_AHALS) throw Unsupported("only the AHALS inner solver runs on the GPU path");
+    if (solver < NTF_SOLVER_AHALS || solver > NTF_SOLVER_ACTIVE_SET) throw LogicError("unknown solver");
     if (rows < 1 || rank < 1) throw InvalidArgument("rows and rank must be >= 1");
     const ntf_inner_stop st = stop ? *stop : ntf_inner_stop{50, 1e-2};
     NTF_CUDA(cudaSetDevice(ctx->device));
@@ -781,7 +783,22 @@ int ntf_solve_nnls(ntf_ctx* ctx, int solver, const double* gram, const double* t
     a.max_iters = st.max_iters;
     a.tol = st.rel_change_tol;
     a.scratch = scratch.as<double>();
-    launch_nnls(a, ctx->stream);
+    DevBuf work, err;
+    if (solver == NTF_SOLVER_AHALS) {
+      launch_nnls(a, ctx->stream);
+    } else {
+      work = DevBuf(2 * n * 8);
+      err = DevBuf(sizeof(int));
+      NTF_CUDA(cudaMemsetAsync(err.p, 0, sizeof(int), ctx->stream));
+      a.solver = solver;
+      a.work = work.as<double>();
+      a.error = err.as<int>();
+      launch_nnls_solver(a, ctx->stream);
+      int e = 0;
+      NTF_CUDA(cudaMemcpyAsync(&e, err.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+      NTF_CUDA(cudaStreamSynchronize(ctx->stream));
+      if (e) throw std::runtime_error(solver_error_message(e));
+    }
     int s = 0;
     NTF_CUDA(cudaMemcpyAsync(out, w.p, n * 8, cudaMemcpyDeviceToHost, ctx->stream));
     NTF_CUDA(cudaMemcpyAsync(&s, sw.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));

@@ -249,9 +249,9 @@ __global__ void __launch_bounds__(TPB, 1) nnls_kernel(NnlsLaunch a) {
   const int sel = F ? F->sel[mode] : 0;
   double* X = F ? F->x[mode][sel] : nullptr;
   const double beta = (a.role == 0) ? st->beta : 0.0;
-  const int max_iters = (a.role == 2) ? a.max_iters : st->inner_max_iters;
+  const int max_iters = (a.role == 2) ? a.max_iters : (a.zero_sweeps ? 0 : st->inner_max_iters);
   const double tol = (a.role == 2) ? a.tol : st->tol;
-  const double* w0 = (a.role == 2) ? a.w0 : X;
+  const double* w0 = (a.role == 2 || a.zero_sweeps) ? a.w0 : X;
   const double* C = a.C;
 
   // ---- G: Hadamard of the other modes' Grams (ones, ascending modes).
@@ -746,7 +746,7 @@ __global__ void __launch_bounds__(kStreamTPB, 1) nnls_stream_kernel(NnlsLaunch a
   if (F) {
     done = st->done;
     beta = (a.role == 0) ? st->beta : 0.0;
-    max_iters = st->inner_max_iters;
+    max_iters = a.zero_sweeps ? 0 : st->inner_max_iters;
     tol = st->tol;
 #pragma unroll
     for (int j = 0; j < kMaxOrder; ++j)
@@ -763,6 +763,29 @@ __global__ void __launch_bounds__(kStreamTPB, 1) nnls_stream_kernel(NnlsLaunch a
   }
   if (done) return;  // budget exhausted: the whole iteration is a no-op (uniform)
   const long long t_begin = clock64();
+  // the last mode's decision scalars, loaded now by the deciding thread so
+  // that no global round trip sits between the final barrier and the record
+  struct Dec {
+    double nsq, f_prev, beta_bar, eta, gamma, gamma_bar, max_time_s;
+    unsigned long long t_start_ns;
+    int k, max_iters, collective_time, sweeps_before;
+  } dec{};
+  const bool decider = F && a.last && blockIdx.x == 0 && threadIdx.x == 0;
+  if (decider) {
+    dec.nsq = st->nsq;
+    dec.f_prev = st->f_prev;
+    dec.beta_bar = st->beta_bar;
+    dec.eta = st->eta;
+    dec.gamma = st->gamma;
+    dec.gamma_bar = st->gamma_bar;
+    dec.max_time_s = st->max_time_s;
+    dec.t_start_ns = st->t_start_ns;
+    dec.k = st->k;
+    dec.max_iters = st->max_iters;
+    dec.collective_time = st->collective_time;
+    for (int j = 0; j < a.order; ++j)
+      if (j != mode) dec.sweeps_before += st->last_sweeps[j];
+  }
 
   const int nrw = int(blockDim.x >> 5) - 1;  // row warps; warp nrw reduces
   const int nloc = nrw * 32 / Q;              // row slots per CTA
@@ -785,7 +808,7 @@ __global__ void __launch_bounds__(kStreamTPB, 1) nnls_stream_kernel(NnlsLaunch a
   unsigned long long* ctl = reinterpret_cast<unsigned long long*>(cbar + kStreamDC);  // (stop << 32) | decided
 
   double* X = sel ? xp1 : xp0;
-  const double* w0 = (a.role == 2) ? a.w0 : X;
+  const double* w0 = (a.role == 2 || a.zero_sweeps) ? a.w0 : X;
   const double* C = a.C;
 
   // rows of C: the first batch of loads is issued before the G loads (both
@@ -855,12 +878,15 @@ __global__ void __launch_bounds__(kStreamTPB, 1) nnls_stream_kernel(NnlsLaunch a
   }
   __syncthreads();
   const long long t_p1 = clock64();
-  double dmax = -INFINITY;
-  for (int j = 0; j < r; ++j) dmax = fmax(dmax, Gs[j * RP + j]);
+  // max diagonal and the updated columns: every warp reads the diagonal once
+  // (lane j < r), a shuffle max and a ballot (r <= 32 here)
+  const int ln = int(threadIdx.x & 31);
+  const double gjj = ln < r ? Gs[ln * RP + ln] : -INFINITY;
+  double dmax = gjj;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
   const double diag_floor = 1e-12 * dmax;  // nnls.cpp:16-19
-  unsigned okbits = 0;                      // columns that are updated (and clipped)
-  for (int j = 0; j < r; ++j)
-    if (Gs[j * RP + j] > diag_floor) okbits |= 1u << j;
+  const unsigned okbits = __ballot_sync(0xffffffffu, ln < r && gjj > diag_floor);  // updated (and clipped) columns
   for (int j = threadIdx.x; j < RP; j += blockDim.x) Ginv[j] = ((okbits >> j) & 1) ? 1.0 / Gs[j * RP + j] : 0.0;
   __syncthreads();
   {
@@ -1032,7 +1058,7 @@ __global__ void __launch_bounds__(kStreamTPB, 1) nnls_stream_kernel(NnlsLaunch a
 #pragma unroll
       for (int l = 0; l < RP; ++l) stp[l] = Wl[l];
     }
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (NTF_NNLS_PROFILE && blockIdx.x == 0 && threadIdx.x == 0) {
       g_nnls_prof[5] += passes;
       g_nnls_prof[6] += pass_cyc;
       g_nnls_prof[7] += gate_cyc;
@@ -1279,8 +1305,10 @@ __global__ void __launch_bounds__(kStreamTPB, 1) nnls_stream_kernel(NnlsLaunch a
     dst[p * r + q] = v;
     dst[q * r + p] = v;
   }
-  double cross = 0.0, quad = 0.0;
-  if (a.last && blockIdx.x == 0 && threadIdx.x == 0) {
+  // <W,C> and <W^T W, G> of the cluster, by CTA 0's last thread while the
+  // others reduce the Grams (remote loads of both in flight together); the
+  // decider reads them after the final cluster barrier
+  if (a.last && blockIdx.x == 0 && threadIdx.x == blockDim.x - 1) {
     double cv[kMaxCluster], qv[kMaxCluster];  // all remote loads in flight before the ordered sums
 #pragma unroll
     for (int c = 0; c < kMaxCluster; ++c) {
@@ -1288,19 +1316,22 @@ __global__ void __launch_bounds__(kStreamTPB, 1) nnls_stream_kernel(NnlsLaunch a
       cv[c] = c < int(ncta) ? pc[2 * RP * RP] : 0.0;
       qv[c] = c < int(ncta) ? pc[2 * RP * RP + 1] : 0.0;
     }
+    double cross = 0.0, quad = 0.0;
 #pragma unroll
     for (int c = 0; c < kMaxCluster; ++c)
       if (c < int(ncta)) {
         cross += cv[c];
         quad += qv[c];
       }
+    red[30] = cross;
+    red[31] = quad;
   }
   const long long t_e4 = clock64();
   drain();
   cl.sync();  // remote reads and every cluster post done before any CTA exits
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
+  if (NTF_NNLS_PROFILE && blockIdx.x == 0 && threadIdx.x == 0) {
     const long long t_end = clock64();
-    unsigned long long* ph = &g_nnls_skew[2][64];  // phase cycles (diagnostics)
+    unsigned long long* ph = &g_nnls_skew[2][64];  // phase cycles (diagnostics, -DNTF_NNLS_PROFILE=1)
     ph[0] += t_p1 - t_begin;
     ph[1] += t_p2 - t_p1;
     ph[2] += t_loop - t_p2;
@@ -1323,28 +1354,28 @@ __global__ void __launch_bounds__(kStreamTPB, 1) nnls_stream_kernel(NnlsLaunch a
     st->last_sweeps[mode] = s;
     return;
   }
-  const double f = 0.5 * st->nsq - cross + 0.5 * quad;
+  const double cross = red[30], quad = red[31];
+  const double f = 0.5 * dec.nsq - cross + 0.5 * quad;
   st->last_sweeps[mode] = s;
-  const int kk = st->k + 1;
-  const double time_s = double(globaltimer() - st->t_start_ns) * 1e-9;
+  const int kk = dec.k + 1;
+  const double time_s = double(globaltimer() - dec.t_start_ns) * 1e-9;
   TraceEntry rec;
   rec.f = f;
   rec.time_s = time_s;
-  rec.sweeps = 0;
-  for (int j = 0; j < a.order; ++j) rec.sweeps += st->last_sweeps[j];
+  rec.sweeps = dec.sweeps_before + s;
   if (a.role == 0) {
-    const bool restarted = f > st->f_prev;  // strict (her.cpp:75)
+    const bool restarted = f > dec.f_prev;  // strict (her.cpp:75)
     if (restarted)
-      for (int j = 0; j < a.order; ++j) F->sel[j] ^= 1;  // X := S for every mode
-    st->f_prev = f;                                      // even on rejection (:84)
-    rec.beta = st->beta;                                 // beta_used
+      for (int j = 0; j < a.order; ++j) F->sel[j] = selv[j] ^ 1;  // X := S for every mode
+    st->f_prev = f;                                                // even on rejection (:84)
+    rec.beta = beta;                                               // beta_used
     rec.restarted = restarted ? 1 : 0;
     if (restarted) {  // update_betas (her.cpp:21-30)
-      st->beta_bar = st->beta;
-      st->beta = __ddiv_rn(st->beta, st->eta);
+      st->beta_bar = beta;
+      st->beta = __ddiv_rn(beta, dec.eta);
     } else {
-      st->beta = fmin(st->beta_bar, __dmul_rn(st->beta, st->gamma));
-      st->beta_bar = fmin(1.0, __dmul_rn(st->beta_bar, st->gamma_bar));
+      st->beta = fmin(dec.beta_bar, __dmul_rn(beta, dec.gamma));
+      st->beta_bar = fmin(1.0, __dmul_rn(dec.beta_bar, dec.gamma_bar));
     }
   } else {
     rec.beta = 0.0;
@@ -1354,8 +1385,8 @@ __global__ void __launch_bounds__(kStreamTPB, 1) nnls_stream_kernel(NnlsLaunch a
   st->f_last = f;
   st->k = kk;
   st->elapsed_s = time_s;
-  if ((st->max_iters > 0 && kk >= st->max_iters) ||
-      (!st->collective_time && st->max_time_s > 0.0 && time_s >= st->max_time_s))
+  if ((dec.max_iters > 0 && kk >= dec.max_iters) ||
+      (!dec.collective_time && dec.max_time_s > 0.0 && time_s >= dec.max_time_s))
     st->done = 1;
 }
 

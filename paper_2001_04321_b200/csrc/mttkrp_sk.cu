@@ -128,25 +128,46 @@ __global__ void __launch_bounds__(32 * (kMaxNP + kMaxMW), 1) mttkrp_sk_kernel(co
     const long long n_units = w1 - w0;
     const long long n_mine = n_units > warp ? (n_units - warp + NP - 1) / NP : 0;
     const int naw = p.naw, DA = p.naw - 1;
-    auto entry = [&](long long jj, int (&e)[kUnitInts]) -> int {  // lane 0: unit-table entry; returns the tile
+    // (tile, unit-in-tile) cursors of the warp's unit stream, advanced by NP
+    // units per step without divisions: one for the TMA issue, one DA units
+    // ahead for the factor-row copies
+    struct Cursor {
+      long long u;
+      int tile;
+    };
+    auto cursor_at = [&](long long jj) {
       const long long w = w0 + warp + jj * NP;
-      const int tile = int(w / U);
-      const int2* src = reinterpret_cast<const int2*>(p.utab + size_t(w - (long long)tile * U) * kUnitInts);
+      Cursor c;
+      c.tile = int(w / U);
+      c.u = w - (long long)c.tile * U;
+      return c;
+    };
+    auto advance = [&](Cursor& c) {
+      c.u += NP;
+      while (c.u >= U) {
+        c.u -= U;
+        ++c.tile;
+      }
+    };
+    auto entry = [&](const Cursor& c, int (&e)[kUnitInts]) {  // lane 0: the unit-table entry
+      const int2* src = reinterpret_cast<const int2*>(p.utab + size_t(c.u) * kUnitInts);
 #pragma unroll
       for (int q = 0; q < kUnitInts / 2; ++q) {
         const int2 x = __ldg(src + q);
         e[2 * q] = x.x;
         e[2 * q + 1] = x.y;
       }
-      return tile;
     };
     // bulk copies of a unit's factor rows into aq slot q, completing on bar
+    // the slot's info area keeps the unit's whole table entry: the TMA issue
+    // of a W-formation unit reads it from shared memory (written DA units
+    // earlier by this lane) instead of a second global round trip
     auto copy_rows = [&](const int (&e)[kUnitInts], int q, uint64_t* bar, bool arm) {
       const int n_valid = e[3], n1 = e[4], kwrap = e[5];
       double* aq = aq_of(q);
       int* info = info_of(q);
-      info[0] = n_valid;
-      info[1] = kwrap;
+#pragma unroll
+      for (int i = 0; i < kUnitInts; ++i) info[i] = e[i];
       const bool wrap = kwrap < KB;
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // earlier generic reads of the slot first
       if (arm) mbar_arrive_expect_tx(bar, unsigned(n_valid + p.nb * (wrap ? 2 : 1)) * row_bytes);
@@ -173,42 +194,65 @@ __global__ void __launch_bounds__(32 * (kMaxNP + kMaxMW), 1) mttkrp_sk_kernel(co
     constexpr int CPL = (8 * NNF + 31) / 32;  // columns per lane
     int s = warp;
     uint32_t round = 0;
-    if (!p.direct_b && lane == 0)
+    Cursor cur = cursor_at(0), ahead = cursor_at(DA);
+    int q_cur = warp * naw, q_ahead = warp * naw + DA;  // aq slots of the two streams
+    uint32_t aq_round = 0;                                // completed trips of q_cur around the ring
+    // lane 0 reads the table entry it needs next one trip early (the global
+    // load's latency hides behind the trip)
+    int nx[kUnitInts];
+    if (!p.direct_b && lane == 0) {
+      Cursor c = cur;
       for (long long jj = 0; jj < DA && jj < n_mine; ++jj) {  // prologue copies
         int e[kUnitInts];
-        entry(jj, e);
-        const int q = warp * naw + int(jj % naw);
-        copy_rows(e, q, &aqb[q], true);
+        entry(c, e);
+        copy_rows(e, warp * naw + int(jj), &aqb[warp * naw + int(jj)], true);
+        advance(c);
       }
+      if (DA < n_mine) entry(ahead, nx);
+    }
+    if (p.direct_b && lane == 0 && n_mine > 0) entry(cur, nx);
     for (long long jj = 0; jj < n_mine; ++jj) {
       __syncwarp();  // every lane's reads of the slot formed last trip precede its refill
-      if (!p.direct_b && lane == 0 && jj + DA < n_mine) {  // rows of a later unit (its slot was formed from)
-        int e[kUnitInts];
-        entry(jj + DA, e);
-        const int q = warp * naw + int((jj + DA) % naw);
-        copy_rows(e, q, &aqb[q], true);
+      if (!p.direct_b && jj + DA < n_mine) {  // rows of a later unit (its slot was formed from)
+        if (lane == 0) copy_rows(nx, q_ahead, &aqb[q_ahead], true);
+        advance(ahead);
+        if (lane == 0 && jj + DA + 1 < n_mine) entry(ahead, nx);
+        if (++q_ahead == (warp + 1) * naw) q_ahead = warp * naw;
       }
       if (round > 0) mbar_wait(&empty[s], (round - 1) & 1);
+      const int tile = cur.tile;
+      advance(cur);
       if (lane == 0) {
-        int e[kUnitInts];
-        const int tile = entry(jj, e);
         if (p.direct_b) {
+          int e[kUnitInts];
+#pragma unroll
+          for (int i = 0; i < kUnitInts; ++i) e[i] = nx[i];
+          if (jj + 1 < n_mine) entry(cur, nx);
           mbar_arrive_expect_tx(&full[s], p.tx_bytes + unsigned(e[3]) * row_bytes);
           tma_unit(e, tile, s);
           copy_rows(e, s, &full[s], false);
         } else {
+          int e[kUnitInts];
+          const int* info = info_of(q_cur);
+#pragma unroll
+          for (int i = 0; i < kUnitInts; ++i) e[i] = info[i];
           mbar_expect_tx(&full[s], p.tx_bytes);
           tma_unit(e, tile, s);
         }
       }
       if (!p.direct_b) {
-        const int q = warp * naw + int(jj % naw);
-        mbar_wait(&aqb[q], uint32_t(jj / naw) & 1u);
+        const int q = q_cur;
+        const uint32_t ph = aq_round & 1u;
+        if (++q_cur == (warp + 1) * naw) {
+          q_cur = warp * naw;
+          ++aq_round;
+        }
+        mbar_wait(&aqb[q], ph);
         double* ws = w_base + size_t(s) * (p.w_stage_bytes / sizeof(double));
         const double* aq = aq_of(q);
         const int* info = info_of(q);
-        const int kmax = info[0];
-        const int kwrap = info[1];
+        const int kmax = info[3];
+        const int kwrap = info[5];
         const bool wrap = kwrap < KB;
 #pragma unroll
         for (int ci = 0; ci < CPL; ++ci) {
@@ -298,8 +342,9 @@ __global__ void __launch_bounds__(32 * (kMaxNP + kMaxMW), 1) mttkrp_sk_kernel(co
     };
     int s = 0;
     uint32_t phase = 0;
-    long long seg0 = w0;
     const int first_tile = int(w0 / U);
+    int tile = first_tile;
+    long long u_in = w0 - (long long)first_tile * U;  // unit index inside the current tile
     for (long long w = w0; w < w1; ++w) {
       mbar_wait(&full[s], phase);
       const unsigned char* ts = t_base + size_t(s) * p.t_stage_bytes;
@@ -332,15 +377,14 @@ __global__ void __launch_bounds__(32 * (kMaxNP + kMaxMW), 1) mttkrp_sk_kernel(co
       for (int f = 0; f < NMF; ++f)
 #pragma unroll
         for (int jn = 0; jn < NNF; ++jn) dmma_8x8x4(acc[f][jn], a1[f], b1[jn]);
-      if ((w + 1) % U == 0 || w + 1 == w1) {
-        const int tile = int(w / U);
+      if (++u_in == U || w + 1 == w1) {
         const int2 cs = reinterpret_cast<const int2*>(tile_ctas)[tile];
         const bool direct = cs.x == cs.y;
         flush(tile, direct, 2 * b + (tile == first_tile ? 0 : 1));
-        seg0 = w + 1;
+        u_in = 0;
+        ++tile;
       }
     }
-    (void)seg0;
   }
   if (!p.n_split) return;
   // ---------------------------------------------------- split-tile reduction
@@ -476,7 +520,7 @@ PFN_cuTensorMapEncodeTiled_v12000 sk_encode_fn() {
   return fn;
 }
 
-constexpr size_t kSkSmem = 200 * 1024;
+constexpr size_t kSkSmem = 222 * 1024;  // of the 227 KB a CTA may claim
 
 }  // namespace
 
@@ -509,7 +553,13 @@ bool sk_choose(const ModeView& v, int dtype, int sms, SkPlan* out) {
   // mw consumer warps of nmf 8-row fragments: 4 warps (one per SM
   // sub-partition) or 8 (two, so one warp's operand loads hide behind the
   // other's DMMAs); NTF_SK_MW / NTF_SK_NMF override.
+  // (measured r02k: tall tile-aligned views gain from 8 -- C2's Y_L pass
+  // 67 -> 57 us -- the others do not)
   int mw = 4;
+  {
+    const long long t8 = (v.I + 127) / 128;  // 128-row tiles of 8 two-fragment warps
+    if (t8 >= 4LL * sms) mw = 8;
+  }
   if (const char* e = std::getenv("NTF_SK_MW")) mw = std::atoi(e) == 8 ? 8 : 4;
   const int rows_per_frag_set = 8 * mw;  // rows per fragment index over the warps
   int nmf = 32 / mw, align = 0;           // 256-row tiles
@@ -562,12 +612,21 @@ bool sk_choose(const ModeView& v, int dtype, int sms, SkPlan* out) {
     p.direct_b = nbase == 0 ? 1 : 0;
     if (const char* e = std::getenv("NTF_SK_DIRECTB")) p.direct_b = p.direct_b && std::atoi(e) != 0;
   }
-  p.naw = 4;  // aq slots per producer warp (copies DA = naw - 1 of its units ahead)
-  if (const char* e = std::getenv("NTF_SK_NAW")) p.naw = std::max(2, std::min(8, std::atoi(e)));
+  // aq slots per producer warp (copies run naw - 1 of its units ahead): 4,
+  // fewer when the T stages would drop below four (C2's 300-row COL view)
   p.w_stage_bytes = p.direct_b ? 0u : unsigned((size_t(sk::kKB) * p.wld * 8 + 127) / 128 * 128);
-  p.aq_stage_bytes = unsigned(((size_t(sk::kKB) + 2 * fast::kMaxBase) * r * 8 + 2 * sizeof(int) + 127) / 128 * 128);
+  p.aq_stage_bytes = unsigned(((size_t(sk::kKB) + 2 * fast::kMaxBase) * r * 8 + fast::kUnitInts * sizeof(int) + 127) /
+                              128 * 128);
   const size_t per_stage = size_t(p.t_stage_bytes) + p.w_stage_bytes + (p.direct_b ? p.aq_stage_bytes : 0u);
-  const size_t fixed = p.direct_b ? 0 : size_t(p.NP) * p.naw * p.aq_stage_bytes;
+  size_t fixed = 0;
+  for (p.naw = 4; p.naw >= 2; --p.naw) {
+    fixed = p.direct_b ? 0 : size_t(p.NP) * p.naw * p.aq_stage_bytes;
+    if ((kSkSmem - fixed) / per_stage >= 4) break;
+  }
+  if (p.naw < 2) p.naw = 2;
+  if (const char* e = std::getenv("NTF_SK_NAW")) p.naw = std::max(2, std::min(8, std::atoi(e)));
+  fixed = p.direct_b ? 0 : size_t(p.NP) * p.naw * p.aq_stage_bytes;
+  if (fixed >= kSkSmem) return false;
   p.stages = int(std::min<size_t>(8, (kSkSmem - fixed) / per_stage));
   if (const char* e = std::getenv("NTF_SK_STAGES")) p.stages = std::min(p.stages, std::max(2, std::atoi(e)));
   p.stages -= p.stages % p.NP;

@@ -71,6 +71,7 @@ struct RunState {
   // (launch_apply_time_budget), so every rank stops at the same iteration
   int collective_time;
   double elapsed_s;
+  int error;  // first inner-solver failure (solver_error_message), 0 = none
 };
 
 struct TraceEntry {
@@ -166,8 +167,21 @@ struct NnlsLaunch {
   const DevFactors* hF;
   DevFactors bufs;
   int has_bufs;
+  // drivers with another inner solver: the block's rows come from w0 (the
+  // solver's result) and no AHALS sweep runs; the kernel only extrapolates,
+  // writes, forms the Grams and (last mode) decides
+  int zero_sweeps;
+  int solver;        // NTF_SOLVER_* (launch_nnls_solver)
+  double* work;      // solver: >= 3 * rows * rank doubles of per-row state
+  int* error;        // solver: first failure code (0 = none), see solver_error_message
 };
 void launch_nnls(const NnlsLaunch& a, cudaStream_t s);
+// PGD / Nesterov / ADMM / active-set (nnls.cpp:51-211) on one thread-block
+// cluster: reads G (Hadamard of the other modes' X-role Grams, or gram_in),
+// C and the warm start (X, or w0), writes the result rows to w_out.
+void launch_nnls_solver(const NnlsLaunch& a, cudaStream_t s);
+// message of a solver failure code (the reference's std::runtime_error texts)
+const char* solver_error_message(int code);
 // diagnostics: {sweep-loop cycles, reduction cycles, sweeps, calls} of CTA 0
 void nnls_prof_read(unsigned long long out[8 + 384], bool reset);
 

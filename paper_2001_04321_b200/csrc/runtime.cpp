@@ -9,6 +9,7 @@
 
 #include <algorithm>
 #include <cstring>
+#include <stdexcept>
 #include <string>
 
 #include "mttkrp_fast.h"
@@ -399,6 +400,10 @@ Session::Session(ntf_ctx* ctx, const ntf_tensor* t, int algo, const double* init
   trace_cap_ = cfg.max_outer_iters > 0 ? cfg.max_outer_iters : (1 << 20);
   trace_ = DevBuf(size_t(trace_cap_) * sizeof(TraceEntry));
   scratch_ = DevBuf(size_t(kNnlsScratch) * sizeof(double));
+  if (cfg.solver != NTF_SOLVER_AHALS) {
+    solve_buf_ = DevBuf(size_t(maxrows) * rank * sizeof(double));
+    solve_work_ = DevBuf(2 * size_t(maxrows) * rank * sizeof(double));
+  }
   dF_ = DevBuf(sizeof(DevFactors));
 
   std::memset(&hF_, 0, sizeof hF_);
@@ -494,6 +499,16 @@ void Session::enqueue_iteration(bool timed) {
     a.scratch = scratch_.as<double>();
     a.bufs = hF_;
     a.has_bufs = 1;
+    if (cfg_.solver != NTF_SOLVER_AHALS) {  // solve_nnls (nnls.cpp:213-222), then the fused epilogue
+      NnlsLaunch b = a;
+      b.solver = cfg_.solver;
+      b.w_out = solve_buf_.as<double>();
+      b.work = solve_work_.as<double>();
+      b.error = &st->error;
+      launch_nnls_solver(b, stream_);
+      a.zero_sweeps = 1;
+      a.w0 = solve_buf_.as<double>();
+    }
     launch_nnls(a, stream_);
   }
   if (collective_time_) {  // every rank applies the same (max) elapsed time
@@ -631,6 +646,13 @@ bool Session::last_record(ntf_trace_record* out) {
   }
   *out = r;
   return true;
+}
+
+void Session::check_error() {
+  int e = 0;
+  NTF_CUDA(cudaMemcpyAsync(&e, &state_.as<RunState>()->error, sizeof(int), cudaMemcpyDeviceToHost, stream_));
+  sync();
+  if (e) throw std::runtime_error(solver_error_message(e));
 }
 
 void Session::set_kernel_timing(bool on) { timing_ = on; }

@@ -155,6 +155,7 @@ class Session {
   void factors(double* out);
   void trace(double* f0, ntf_trace_record* out, int cap, int* n);
   bool last_record(ntf_trace_record* out);  // the newest trace record (false: none yet)
+  void check_error();  // throws the inner solver's failure (std::runtime_error in the reference)
   void set_kernel_timing(bool on);
   void kernel_times(double* ms_per_mode, int* launches, int* total_kernels);
   cudaStream_t stream() const { return stream_; }
@@ -174,6 +175,7 @@ class Session {
   std::unique_ptr<MttkrpEngine> eng_;
   DevFactors hF_{};
   DevBuf dF_, fac_, fac32_, grams_, C_, state_, trace_, scratch_, counter_;
+  DevBuf solve_buf_, solve_work_;  // another inner solver: its result rows and per-row state
   int trace_cap_ = 0;
   cudaGraph_t graph_ = nullptr;
   cudaGraphExec_t exec_ = nullptr;

@@ -288,8 +288,8 @@ def test_driver_validation(P):
     bad[0][0, 0] = -1.0
     with pytest.raises(ValueError):
         P.her_run(t, bad, P.AoConfig(max_outer_iters=3))
-    with pytest.raises(P.UnsupportedError):
-        P.her_run(t, init, P.AoConfig(solver=P.NnlsSolver.admm, max_outer_iters=3))
+    with pytest.raises(P.LogicError, match="unknown solver"):
+        P.her_run(t, init, P.AoConfig(solver=7, max_outer_iters=3))
 
 
 def test_too_tall_factor_is_refused_up_front(P):

@@ -136,10 +136,42 @@ def test_cpp_header_api_compiles_and_runs(P, tmp_path, oracle):
     subprocess.run(["g++", "-std=c++17", "-O1", "-I", os.path.join(ROOT, "include"),
                     os.path.join(ROOT, "tests", "cpp", "api_smoke.cpp"), "-L", libdir, "-l:libntf_b200.so",
                     f"-Wl,-rpath,{libdir}", "-o", str(exe)], check=True)
-    out = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout
+    out = subprocess.run([str(exe), "cpu", str(tmp_path / "smoke.ntfk")], capture_output=True, text=True,
+                         check=True).stdout
     t, _ = oracle.generate([6, 5, 4], 3, 0.1, False, 42)
     init = oracle.random_init([6, 5, 4], 3, oracle.stream_seed(42, 1))
-    assert f"sum={float(np.sum(t)):.17g}" != "" and "init00=%.17g" % init[0][0, 0] in out
+    seq = 0.0  # the C++ side sums in flat order
+    for x in t.ravel():
+        seq += float(x)
+    assert f"sum={seq:.17g} init00={init[0][0, 0]:.17g}" in out, out
+    assert "ntfk roundtrip ok" in out
+    back = P.TuckerFormat.load(str(tmp_path / "smoke.ntfk"))  # the C++ writer's container, read by Python
+    assert np.array_equal(back.core, t) and all(np.array_equal(b, np.eye(d)) for b, d in zip(back.bases, (6, 5, 4)))
+
+
+@pytest.mark.gpu
+def test_cpp_header_drivers_on_gpu(P, tmp_path):
+    """The GPU branch of tests/cpp/api_smoke.cpp: ntfb::her_run through the
+    C++ header on a GpuDenseProvider gives the same bits as the Python API
+    on the same inputs; on a TuckerProvider (identity bases) the same trace
+    to 1e-8."""
+    import subprocess
+    from paper_2001_04321_b200 import _lib
+    exe = tmp_path / "api_smoke"
+    libdir = os.path.dirname(_lib.LIB_PATH)
+    subprocess.run(["g++", "-std=c++17", "-O1", "-I", os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "tests", "cpp", "api_smoke.cpp"), "-L", libdir, "-l:libntf_b200.so",
+                    f"-Wl,-rpath,{libdir}", "-o", str(exe)], check=True)
+    out = subprocess.run([str(exe), "gpu", str(tmp_path / "s.ntfk")], capture_output=True, text=True,
+                         check=True).stdout
+    spec = P.SyntheticSpec(shape=[6, 5, 4], rank=3, noise_sigma=0.1, seed=42)
+    t, _ = P.generate(spec)
+    init = P.random_init([6, 5, 4], 3, P.stream_seed(42, 1))
+    _, tr = P.her_run(t, init, P.AoConfig(max_outer_iters=10), P.HerParams())
+    assert f"f0={tr.f0:.17g} f10={tr.final_f():.17g} restarts={tr.restart_count()}" in out, out
+    line = [ln for ln in out.splitlines() if ln.startswith("tucker ")][0]
+    f10 = float(line.split("f10=")[1].split()[0])
+    assert abs(f10 - tr.final_f()) <= 1e-8 * abs(tr.final_f())
 
 
 def test_no_cpu_fallback_without_device(P):
