@@ -598,6 +598,10 @@ bool sk_choose(const ModeView& v, int dtype, int sms, SkPlan* out) {
   }
   p.n_tiles = int((v.I + m_cta - 1) / m_cta);
   p.W = (long long)p.n_tiles * p.U;
+  // a single-tile COL view (C2's block N-1 pass: 300 rows, K split over every
+  // SM) stays on the k-split fast kernel: measured r02n/r02o, 75 us there
+  // against 75-90 us here across stage / producer / warp counts
+  if (layout == fast::kCol && p.n_tiles == 1 && !std::getenv("NTF_SK_FORCE")) return false;
   p.align = align && p.n_tiles >= sms ? 1 : 0;
   p.tx_bytes = p.t_stage_bytes;
   // no base modes (a single varying factor, e.g. the dimension tree's Y_L

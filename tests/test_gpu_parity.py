@@ -133,8 +133,10 @@ def test_ahals_basic_properties(P, oracle):
     # fixed point stops early
     c = gen.uniform(-1, 1, (4, 3))
     assert np.array_equal(P.solve_nnls(0, np.eye(3), c, np.maximum(c, 0), P.InnerStop(50, 1e-2)), np.maximum(c, 0))
-    with pytest.raises(P.UnsupportedError):
-        P.solve_nnls(P.NnlsSolver.admm, np.eye(3), c, np.maximum(c, 0))
+    # every solver keeps a fixed point of the NNLS (nnls.cpp:51-211 on the GPU)
+    for solver in (P.NnlsSolver.admm, P.NnlsSolver.pgd, P.NnlsSolver.nesterov, P.NnlsSolver.active_set):
+        got = P.solve_nnls(solver, np.eye(3), c, np.maximum(c, 0))
+        assert np.abs(got - np.maximum(c, 0)).max() <= 1e-14
 
 
 @pytest.mark.parametrize("rows,r", [(4, 2), (6, 3), (300, 20), (500, 32), (100, 16), (2000, 64), (1100, 10)])
