@@ -317,11 +317,8 @@ def run_ours(args):
     # Y_L (timed at block 0) and Y_R (block h; h = N-1 for 3-way: block N-1's
     # own MTTKRP), each timed alone -- the other blocks' per_mode_ms are their
     # tree contractions
-    split = tree_split(len(shape))
-    if args.dimtree:
-        avg_ms = (per_mode_ms[0] + per_mode_ms[split]) / 2
-    else:
-        avg_ms = sum(kms) / max(sum(kcnt), 1)
+    slots = sess.pass_slots()  # which timing slots hold full tensor passes
+    avg_ms = sum(per_mode_ms[i] for i in slots) / len(slots)
     local_shape = list(t_local.shape)
     bytes_per = P.mttkrp_bytes(local_shape, r, itemsize)
     flops_per = P.mttkrp_flops(local_shape, r)
@@ -386,8 +383,10 @@ def run_ours(args):
             "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm_peak, "unit": "GB/s",
                          "frac": achieved_gbs / hbm_peak, "traffic": traffic, "peak_kind": peak_kind,
                          "traffic_source": "profiles/traffic.json (ncu dram__bytes_read+write per launch)",
-                         "kernel": (f"MTTKRP full tensor passes (Y_L at block 0, Y_R at block {split}; dimension tree on)" if args.dimtree
+                         "kernel": ("MTTKRP full tensor passes of an outer iteration (dimension tree: Y_L at block 0 "
+                                    "and the second partial; each timed alone)" if args.dimtree
                                     else "MTTKRP (main kernel, avg over modes)"),
+                         "pass_slots": slots,
                          "bytes_per_launch": bytes_per, "avg_launch_ms": avg_ms,
                          "per_mode_ms": per_mode_ms,
                          "fma_tflops": flops_per / (avg_ms / 1e3) / 1e12,

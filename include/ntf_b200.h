@@ -70,6 +70,8 @@ typedef struct {
 #define NTF_RUN_NO_GRAPH 2u /* launch kernels directly instead of a CUDA graph */
 #define NTF_RUN_GENERIC 4u  /* force the generic MTTKRP kernel (testing)     */
 #define NTF_RUN_DIRECT 8u   /* N full MTTKRP passes per iteration (no tree)   */
+#define NTF_RUN_NO_OVERLAP 16u /* 3-way: keep block N-1's pass on the critical
+                                  path instead of beside block 1's NNLS      */
 
 /* AoConfig (include/ntf/ao.hpp:15-24). `ground_truth` is a concatenated
  * factor model (same shape and rank as the init) and is required when
@@ -303,6 +305,10 @@ int ntf_session_trace(ntf_session* s, double* f0, ntf_trace_record* trace, int c
 int ntf_session_set_kernel_timing(ntf_session* s, int on);
 int ntf_session_kernel_times(ntf_session* s, double* ms_per_mode, int* launches_per_mode,
                              int* kernel_launches_total);
+/* Which per-mode timing slots of ntf_session_kernel_times hold the outer
+ * iteration's full tensor passes (the rest are dimension-tree contractions):
+ * slots[0..n), n <= order. */
+int ntf_session_pass_slots(ntf_session* s, int* slots, int* n);
 int ntf_session_destroy(ntf_session* s);
 
 #ifdef __cplusplus

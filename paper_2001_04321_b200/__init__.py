@@ -11,7 +11,7 @@ from . import _lib
 _lib.lib()  # fail loudly when the CUDA extension is not built
 
 from .api import (  # noqa: E402,F401
-    RUN_DIMTREE, RUN_DIRECT, RUN_GENERIC, RUN_NO_GRAPH, AoConfig, Context, CudaError, GpuDenseProvider, HerIterationInfo, HerParams, HerState, InnerStop,
+    RUN_DIMTREE, RUN_DIRECT, RUN_GENERIC, RUN_NO_GRAPH, RUN_NO_OVERLAP, AoConfig, Context, CudaError, GpuDenseProvider, HerIterationInfo, HerParams, HerState, InnerStop,
     InvalidArgument, KruskalModel, LogicError, NcclError, NnlsSolver, ObjectiveProvider, RunTrace, Session,
     SyntheticSpec, TraceRecord, UnsupportedError, ahals_solve, ao_run, default_context, device_count,
     factor_error, generate, her_run, load_tensor, mttkrp_bytes, mttkrp_flops, nnls_solver_from_name, ntft_info,

@@ -28,6 +28,7 @@ NTF_RUN_DIMTREE = 1
 NTF_RUN_NO_GRAPH = 2
 NTF_RUN_GENERIC = 4
 NTF_RUN_DIRECT = 8
+NTF_RUN_NO_OVERLAP = 16
 
 dptr = C.POINTER(C.c_double)
 iptr = C.POINTER(C.c_int)
@@ -123,6 +124,7 @@ SIGNATURES = {
     "ntf_session_trace": (C.c_int, [C.c_void_p, dptr, C.POINTER(TraceRecordC), C.c_int, iptr]),
     "ntf_session_set_kernel_timing": (C.c_int, [C.c_void_p, C.c_int]),
     "ntf_session_kernel_times": (C.c_int, [C.c_void_p, dptr, iptr, iptr]),
+    "ntf_session_pass_slots": (C.c_int, [C.c_void_p, iptr, iptr]),
     "ntf_session_destroy": (C.c_int, [C.c_void_p]),
 }
 

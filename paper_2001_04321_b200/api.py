@@ -97,6 +97,7 @@ RUN_DIMTREE = 1   # accepted for compatibility: the tree is the default
 RUN_NO_GRAPH = 2  # enqueue every iteration directly (no CUDA graph)
 RUN_GENERIC = 4   # generic MTTKRP kernel only (diagnostics)
 RUN_DIRECT = 8    # N full MTTKRP passes per iteration (the reference's loop shape)
+RUN_NO_OVERLAP = 16  # 3-way: block N-1's pass on the critical path, not beside block 1's NNLS
 
 
 @dataclasses.dataclass
@@ -918,6 +919,13 @@ class Session:
         tot = C.c_int()
         _check(L.lib().ntf_session_kernel_times(self.handle, ms, cnt, C.byref(tot)))
         return list(ms), list(cnt), tot.value
+
+    def pass_slots(self):
+        """Timing slots of kernel_times() that hold full tensor passes."""
+        slots = (C.c_int * 8)()
+        n = C.c_int()
+        _check(L.lib().ntf_session_pass_slots(self.handle, slots, C.byref(n)))
+        return [slots[i] for i in range(n.value)]
 
     def close(self):
         if getattr(self, "handle", None):

@@ -900,6 +900,15 @@ int ntf_session_kernel_times(ntf_session* s, double* ms_per_mode, int* launches_
   });
 }
 
+int ntf_session_pass_slots(ntf_session* s, int* slots, int* n) {
+  return guarded([&] {
+    need(s, "session");
+    need(slots, "slots");
+    need(n, "n");
+    *n = SESSION(s)->pass_slots(slots);
+  });
+}
+
 // Diagnostics (not part of the public header): CTA-0 cycle counters of the
 // NNLS kernel {sweep-loop cycles, reduction cycles, sweeps, calls}.
 int ntf_debug_nnls_prof(unsigned long long* out, int reset) {

@@ -235,6 +235,7 @@ __global__ void __launch_bounds__(TPB, 1) nnls_kernel(NnlsLaunch a) {
   cg::cluster_group cl = cg::this_cluster();
 
   RunState* st = a.st;
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // see nnls_stream_kernel
   if (st && st->done) return;  // budget exhausted: the whole iteration is a no-op (uniform)
 
   const int r = a.rank, mode = a.mode;
@@ -761,6 +762,9 @@ __global__ void __launch_bounds__(kStreamTPB, 1) nnls_stream_kernel(NnlsLaunch a
     for (int j = 0; j < kMaxOrder; ++j)
       if (j == mode) sel = selv[j];
   }
+  // a programmatic dependent (the overlapped tensor pass) may start now, on
+  // the SMs this cluster leaves free: it reads nothing this kernel writes
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (done) return;  // budget exhausted: the whole iteration is a no-op (uniform)
   const long long t_begin = clock64();
   // the last mode's decision scalars, loaded now by the deciding thread so

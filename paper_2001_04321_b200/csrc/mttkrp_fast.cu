@@ -310,7 +310,7 @@ std::vector<int> fast_mttkrp_unit_table(const ModeView& v, int dtype, int sms) {
 }
 
 void fast_mttkrp(const void* t, int dtype, const ModeView& v, const DevFactors* dF, const int* unit_table,
-                 double* partial, double* out, int sms, cudaStream_t s, unsigned* counter) {
+                 double* partial, double* out, int sms, cudaStream_t s, unsigned* counter, bool pdl) {
   Choice ch;
   if (!choose(v, dtype, sms, &ch)) throw Unsupported("no fast MTTKRP plan for this view");
   if (!unit_table) throw LogicError("fast MTTKRP needs its unit table");
@@ -319,7 +319,7 @@ void fast_mttkrp(const void* t, int dtype, const ModeView& v, const DevFactors* 
     if (sk_choose(v, dtype, sms, &sp) && sp.layout == ch.layout) {
       fast::Params modes{};
       fill_params_modes(v, sp.layout, modes);
-      sk_mttkrp(t, v, sp, dF, unit_table, partial, out, s, counter, modes);
+      sk_mttkrp(t, v, sp, dF, unit_table, partial, out, s, counter, modes, pdl);
       return;
     }
   }
@@ -334,6 +334,7 @@ void fast_mttkrp(const void* t, int dtype, const ModeView& v, const DevFactors* 
   ch.p.counter = nullptr;
   if (!direct && counter && !std::getenv("NTF_FAST_SEPARATE_REDUCE")) ch.p.counter = counter;
   ch.p.utab = unit_table;
+  ch.p.pdl = pdl && !ch.p.counter ? 1 : 0;  // (a cooperative split-K launch is never a dependent)
   fill_params_modes(v, ch.layout, ch.p);
   // FP32 register sums over more than ~16k terms drift past the 1e-5
   // relative bar at BASELINE config 5 (1.05e-5 measured at 2000^3, r = 64)

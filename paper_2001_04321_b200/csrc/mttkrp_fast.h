@@ -20,7 +20,9 @@ size_t fast_mttkrp_partial_len(const ModeView& v, int dtype, int sms);
 std::vector<int> fast_mttkrp_unit_table(const ModeView& v, int dtype, int sms);
 // `counter` (zeroed device word owned by the caller, used by one stream at a
 // time) enables the in-kernel split-K reduction; nullptr: separate kernel.
+// pdl: launch as a programmatic dependent of the previous kernel in the
+// stream (it may start while that kernel runs, on the SMs it leaves free).
 void fast_mttkrp(const void* t, int dtype, const ModeView& v, const DevFactors* dF, const int* unit_table,
-                 double* partial, double* out, int sms, cudaStream_t s, unsigned* counter = nullptr);
+                 double* partial, double* out, int sms, cudaStream_t s, unsigned* counter = nullptr, bool pdl = false);
 
 }  // namespace ntfb

@@ -58,6 +58,7 @@ struct Params {
   // CTA's FP64 slab and restarts them, so no FP32 sum runs over more than
   // flush_units * kbox terms (0: accumulate the whole range in registers)
   int flush_units;
+  int pdl;  // host only: launch as a programmatic dependent
 };
 using LaunchFn = void (*)(const CUtensorMap& map, const Params& p, int grid, int threads, size_t smem,
                           cudaStream_t s);

@@ -465,11 +465,13 @@ void launch_sk(const CUtensorMap& map, const SkParams& p, int grid, int threads,
   cfg.blockDim = dim3(unsigned(threads));
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeCooperative;  // the split-tile reduction waits for every CTA
   attr[0].val.cooperative = p.n_split ? 1 : 0;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = p.pdl ? 1 : 0;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   NTF_CUDA(cudaLaunchKernelEx(&cfg, fn, map, p));
 }
 
@@ -679,7 +681,8 @@ void sk_append_tables(const SkPlan& pl, std::vector<int>* tab) {
 }
 
 void sk_mttkrp(const void* t, const ModeView& v, const SkPlan& pl, const DevFactors* dF, const int* unit_table,
-               double* partial, double* out, cudaStream_t s, unsigned* counter, const fast::Params& modes) {
+               double* partial, double* out, cudaStream_t s, unsigned* counter, const fast::Params& modes,
+               bool pdl) {
   auto fn = sk_encode_fn();
   if (!fn) throw CudaError("cuTensorMapEncodeTiled is unavailable");
   const SkParams& p0 = pl.p;
@@ -722,6 +725,7 @@ void sk_mttkrp(const void* t, const ModeView& v, const SkPlan& pl, const DevFact
   for (int q = 0; q < fast::kMaxBase; ++q) p.bq[q] = modes.bq[q];
   p.qL = modes.qL;
   p.rowL_wrap = modes.rowL_wrap;
+  p.pdl = pdl && !p.n_split ? 1 : 0;  // (a cooperative split-tile launch is never a dependent)
   if (p.n_split && !counter) throw LogicError("stream-K MTTKRP needs an arrival counter");
   sk::pick(pl.nmf, pl.nnf, pl.layout)(map, p, pl.grid, pl.threads, pl.smem, s);
 }

@@ -27,6 +27,7 @@ struct SkParams {
   int lpo;    // split-tile reduction: lanes per output (1, or 8 for wide fan-in)
   int direct_b;  // no base modes: DMMA B operand = the bulk-copied factor rows (no W formation)
   int naw;       // W formation: aq slots per producer warp
+  int pdl;       // host only: launch as a programmatic dependent
   int m_box, n_mbox, m_cta, m_pitch;
   int MW, NP, stages, wld;
   unsigned t_stage_bytes, w_stage_bytes, aq_stage_bytes, tx_bytes;
@@ -46,7 +47,8 @@ bool sk_choose(const ModeView& v, int dtype, int sms, SkPlan* out);
 size_t sk_partial_len(const ModeView& v, int dtype, int sms);
 void sk_append_tables(const SkPlan& pl, std::vector<int>* tab);
 void sk_mttkrp(const void* t, const ModeView& v, const SkPlan& pl, const DevFactors* dF, const int* unit_table,
-               double* partial, double* out, cudaStream_t s, unsigned* counter, const fast::Params& modes);
+               double* partial, double* out, cudaStream_t s, unsigned* counter, const fast::Params& modes,
+               bool pdl = false);
 std::string sk_describe(const SkPlan& pl);
 
 }  // namespace ntfb

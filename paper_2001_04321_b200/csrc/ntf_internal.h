@@ -15,6 +15,7 @@ namespace ntfb {
 constexpr int kMaxOrder = NTF_MAX_ORDER;
 constexpr int kMaxRank = 64;  // largest r served by the fused NNLS kernel
 constexpr int kMaxNnlsRows = 16 * 256;  // largest factor height it serves (one 16-CTA cluster)
+constexpr int kNnlsReserveSms = 16;      // SMs a concurrent pass leaves to the NNLS cluster
 
 // ---- errors ----------------------------------------------------------------
 // Host code throws these; the C ABI maps them to status codes.

@@ -210,6 +210,23 @@ MttkrpEngine::MttkrpEngine(const ntf_ctx* ctx, const ntf_tensor* t, int rank, un
       NTF_CUDA(cudaMemcpy(ttm_tab_.p, tab.data(), tab.size() * sizeof(int), cudaMemcpyHostToDevice));
       ybuf_ = DevBuf(size_t(ttm_view_.I) * rank * sizeof(double));
       need = std::max(need, fast_mttkrp_partial_len(ttm_view_, t->dtype, ctx->sms));
+      if (N == 3 && h == N - 1 && !t->rows_only && !(flags & NTF_RUN_NO_OVERLAP)) {
+        const char* oe = std::getenv("NTF_OVERLAP");
+        if (!(oe && std::atoi(oe) == 0)) {
+          const int osms = std::max(1, ctx->sms - kNnlsReserveSms);
+          const ModeView pv = right_view(1);
+          const std::vector<int> ptab = fast_mttkrp_unit_table(pv, t->dtype, osms);
+          if (!ptab.empty()) {
+            overlap_ = true;
+            p0_sms_ = osms;
+            p0_view_ = pv;
+            p0_tab_ = DevBuf(ptab.size() * sizeof(int));
+            NTF_CUDA(cudaMemcpy(p0_tab_.p, ptab.data(), ptab.size() * sizeof(int), cudaMemcpyHostToDevice));
+            p0buf_ = DevBuf(size_t(pv.I) * rank * sizeof(double));
+            need = std::max(need, fast_mttkrp_partial_len(pv, t->dtype, osms));
+          }
+        }
+      }
       if (h < N - 1) {
         ttmr_view_ = right_view(h);
         ttmr_tab_ = DevBuf(rtab.size() * sizeof(int));
@@ -259,9 +276,23 @@ MttkrpEngine::MttkrpEngine(const ntf_ctx* ctx, const ntf_tensor* t, int rank, un
 }
 
 TreeView MttkrpEngine::tree_view(int mode) const {
+  const ModeView v = view(mode);
+  if (overlap_ && mode == order_ - 1) {  // P_0: (i1, i2) rows, contract i1 with A_1
+    TreeView y{};
+    y.order = 2;
+    y.mode = 1;
+    y.rank = rank_;
+    y.dims[0] = v.dims[1];
+    y.dims[1] = v.dims[2];
+    y.L = v.dims[1];
+    y.I = v.dims[2];
+    y.R = 1;
+    y.row0 = 0;
+    y.foff = 1;
+    return y;
+  }
   // blocks < split_: Y_L over modes 0..split_-1; blocks >= split_: Y_R over
   // modes split_..N-1 (factor offset split_, no slab offset)
-  const ModeView v = view(mode);
   const bool left = mode < split_;
   const int lo = left ? 0 : split_, hi = left ? split_ : t_->order;
   TreeView y{};
@@ -334,10 +365,24 @@ void MttkrpEngine::run(int mode, const DevFactors* dF, double* out, cudaStream_t
     // kernel timing (ev0/ev1): a block that forms a partial times that full
     // tensor pass alone, the other blocks time their tree contraction
     bool pass = false;
+    if (overlap_ && mode == order_ - 1) {  // block 2 from P_0 (formed after block 1's NNLS)
+      if (!p0_ready_) {  // reached out of sweep order: form it now
+        fast_mttkrp(t_->data.p, t_->dtype, p0_view_, dF, p0_tab_.as<int>(), partial_.as<double>(),
+                    p0buf_.as<double>(), p0_sms_, s, counter_.as<unsigned>());
+        pass = true;
+      }
+      p0_ready_ = false;
+      if (ev1 && pass) NTF_CUDA(cudaEventRecord(ev1, s));
+      launch_tree_mttkrp(p0buf_.as<double>(), tree_view(mode), dF, partial_.as<double>(), tree_chunks_[mode],
+                         tree_arrivals_.as<unsigned>(), dst, s);
+      if (ev1 && !pass) NTF_CUDA(cudaEventRecord(ev1, s));
+      goto exchange;
+    }
     if (mode == 0 || (mode < split_ && !seq)) {
       fast_mttkrp(t_->data.p, t_->dtype, ttm_view_, dF, ttm_tab_.as<int>(), partial_.as<double>(), ybuf_.as<double>(),
                   ctx_->sms, s, counter_.as<unsigned>());
       pass = true;
+      p0_ready_ = false;  // a new sweep starts: P_0 of the previous one is stale
     }
     if (mode == split_ || (mode > split_ && !seq)) {
       fast_mttkrp(t_->data.p, t_->dtype, ttmr_view_, dF, ttmr_tab_.as<int>(), partial_.as<double>(),
@@ -357,6 +402,7 @@ void MttkrpEngine::run(int mode, const DevFactors* dF, double* out, cudaStream_t
     if (ev1) NTF_CUDA(cudaEventRecord(ev1, s));
     launch_reduce_partials(partial_.as<double>(), segs_[mode], v.I * rank_, dst, s);
   }
+exchange:
   if (!comm.active()) return;
   if (gather) {
     comm.allgather(gather_.as<double>(), size_t(maxrows_) * rank_, s);
@@ -365,6 +411,16 @@ void MttkrpEngine::run(int mode, const DevFactors* dF, double* out, cudaStream_t
   } else {
     comm.allreduce_sum(out, size_t(v.I) * rank_, s);
   }
+}
+
+void MttkrpEngine::after_block(int mode, const DevFactors* dF, cudaStream_t s, bool pdl, cudaEvent_t ev0,
+                               cudaEvent_t ev1) {
+  if (!overlap_ || mode != 1) return;
+  if (ev0) NTF_CUDA(cudaEventRecord(ev0, s));
+  fast_mttkrp(t_->data.p, t_->dtype, p0_view_, dF, p0_tab_.as<int>(), partial_.as<double>(), p0buf_.as<double>(),
+              p0_sms_, s, counter_.as<unsigned>(), pdl);
+  if (ev1) NTF_CUDA(cudaEventRecord(ev1, s));
+  p0_ready_ = true;
 }
 
 // ---- Session -------------------------------------------------------------------
@@ -510,6 +566,22 @@ void Session::enqueue_iteration(bool timed) {
       a.w0 = solve_buf_.as<double>();
     }
     launch_nnls(a, stream_);
+    if (eng_->overlap() && i == 1) {
+      // the overlapped pass: launched right after block 1's NNLS as its
+      // programmatic dependent (timing runs serialise it to time it alone;
+      // its events replace block 1's contraction slot)
+      cudaEvent_t p0 = nullptr, p1 = nullptr;
+      if (timed) {
+        NTF_CUDA(cudaEventCreate(&p0));
+        NTF_CUDA(cudaEventCreate(&p1));
+        ev_.push_back(p0);
+        ev_.push_back(p1);
+        ev_mode_.push_back(i);
+        // drop block 1's contraction timing (its slot now holds the pass)
+        ev_mode_[ev_mode_.size() - 2] = -1;
+      }
+      eng_->after_block(i, dF, stream_, !timed, p0, p1);
+    }
   }
   if (collective_time_) {  // every rank applies the same (max) elapsed time
     ctx_->comm.allreduce_max(&st->elapsed_s, 1, stream_);
@@ -660,6 +732,7 @@ void Session::set_kernel_timing(bool on) { timing_ = on; }
 void Session::kernel_times(double* ms_per_mode, int* launches, int* total_kernels) {
   sync();
   for (size_t k = 0; k < ev_mode_.size(); ++k) {
+    if (ev_mode_[k] < 0) continue;
     float ms = 0.f;
     NTF_CUDA(cudaEventElapsedTime(&ms, ev_[2 * k], ev_[2 * k + 1]));
     kernel_ms_[ev_mode_[k]] += ms;

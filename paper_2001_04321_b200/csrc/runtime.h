@@ -89,6 +89,16 @@ class MttkrpEngine {
   void run(int mode, const DevFactors* dF, double* out, cudaStream_t s, cudaEvent_t ev0 = nullptr,
            cudaEvent_t ev1 = nullptr);
   int kernels_per_call(int mode) const;
+  // Work enqueued after block `mode`'s NNLS kernel: with the overlapped
+  // 3-way tree (below) the partial P_0 = T x_0 A_0 of block 2 after block
+  // 1's NNLS, as a programmatic dependent launch (pdl) so it runs on the SMs
+  // the NNLS leaves free. ev0/ev1 (timing) bracket it when launched.
+  void after_block(int mode, const DevFactors* dF, cudaStream_t s, bool pdl, cudaEvent_t ev0 = nullptr,
+                   cudaEvent_t ev1 = nullptr);
+  bool overlap() const { return overlap_; }
+  // timing slots that hold full tensor passes (Y_L at block 0; the second
+  // pass: P_0 after block 1 when overlapped, else block h's)
+  int second_pass_slot() const { return overlap_ ? 1 : split_; }
   ModeView view(int mode) const;
   std::string describe(int mode) const;
   // Dimension tree (NTF_RUN_DIMTREE, order >= 3, fast plans for the partials):
@@ -116,7 +126,18 @@ class MttkrpEngine {
   DevBuf ttmr_tab_, yrbuf_;      // its unit table; Y_R (partial over the local slab, FP64)
   int order_ = 0;
   int last_mode_ = -1;           // previous run() block (a tree partial is reused only in sweep order)
-  bool tree_mode(int mode) const { return tree_ && (mode < split_ || split_ < order_ - 1); }
+  bool tree_mode(int mode) const {
+    return tree_ && (mode < split_ || split_ < order_ - 1 || (overlap_ && mode == order_ - 1));
+  }
+  // Overlapped 3-way tree: blocks 0 and 1 contract Y_L = T x_2 A_2 as before;
+  // block 2 contracts P_0 = T x_0 A_0 (rows (i1, i2)) with A_1. P_0 needs only
+  // block 0's new factor, so its full tensor pass runs beside block 1's NNLS
+  // (16 SMs) on the other SMs instead of on the critical path.
+  bool overlap_ = false;
+  bool p0_ready_ = false;
+  int p0_sms_ = 0;
+  ModeView p0_view_{};
+  DevBuf p0_tab_, p0buf_;
   DevBuf counter_;               // arrival counter of the in-kernel split-K reduction
   int tree_chunks_[kMaxOrder] = {};
   int tree_tiles_max_ = 1;
@@ -159,6 +180,16 @@ class Session {
   void set_kernel_timing(bool on);
   void kernel_times(double* ms_per_mode, int* launches, int* total_kernels);
   cudaStream_t stream() const { return stream_; }
+  // timing slots (per-mode) holding the iteration's full tensor passes
+  int pass_slots(int* slots) const {
+    if (!eng_->tree()) {
+      for (int i = 0; i < order_; ++i) slots[i] = i;
+      return order_;
+    }
+    slots[0] = 0;
+    slots[1] = eng_->second_pass_slot();
+    return 2;
+  }
   int order() const { return order_; }
 
  private:
