@@ -145,7 +145,9 @@ static void check_model(const std::vector<int>& shape, const Model& m) {
 // (ascending right), then acc += wl[left,:] .* inner.
 // Summation-order variant (conditioning experiments only, tools/r02/
 // oracle_sensitivity.py): 1 walks `left` and `right` in descending order -- the
-// same algorithm, rounded differently. 0 (default) is the reference's order.
+// same algorithm, rounded differently; 2 rounds the Khatri-Rao rows to float
+// (what FP32 factor mirrors do to an FP32 tensor's MTTKRP). 0 (default) is the
+// reference's order.
 int g_sum_order = 0;
 
 template <typename T>
@@ -157,18 +159,22 @@ Mat mttkrp(const T* data, const std::vector<int>& shape, const Model& m, int mod
   std::vector<const Mat*> lows, highs;
   for (int l = 0; l < mode; ++l) lows.push_back(&m[size_t(l)]);
   for (int l = mode + 1; l < n; ++l) highs.push_back(&m[size_t(l)]);
-  const Mat wl = lows.empty() ? Mat(1, r, 1.0) : khatri_rao(lows);
-  const Mat wr = highs.empty() ? Mat(1, r, 1.0) : khatri_rao(highs);
+  Mat wl = lows.empty() ? Mat(1, r, 1.0) : khatri_rao(lows);
+  Mat wr = highs.empty() ? Mat(1, r, 1.0) : khatri_rao(highs);
+  if (g_sum_order == 2) {  // FP32-mirror emulation: Khatri-Rao rows rounded to float (conditioning experiments)
+    for (double& x : wl.v) x = double(float(x));
+    for (double& x : wr.v) x = double(float(x));
+  }
   Mat out(s.mid, r);
 #pragma omp parallel for schedule(static)
   for (int64_t mid = 0; mid < s.mid; ++mid) {
     std::vector<double> acc(static_cast<size_t>(r), 0.0), inner(static_cast<size_t>(r));
     for (int64_t li = 0; li < s.left; ++li) {
-      const int64_t left = g_sum_order ? s.left - 1 - li : li;
+      const int64_t left = g_sum_order == 1 ? s.left - 1 - li : li;
       const T* src = data + (left * s.mid + mid) * s.right;
       std::fill(inner.begin(), inner.end(), 0.0);
       for (int64_t ri = 0; ri < s.right; ++ri) {
-        const int64_t right = g_sum_order ? s.right - 1 - ri : ri;
+        const int64_t right = g_sum_order == 1 ? s.right - 1 - ri : ri;
         const double t = double(src[right]);
         const double* w = &wr.v[size_t(right * r)];
         for (int64_t c = 0; c < r; ++c) inner[size_t(c)] += t * w[c];

@@ -714,9 +714,15 @@ __device__ __forceinline__ unsigned long long ld_volatile_u64(const unsigned lon
 // okm == 0 (skipped column): sign-bit masking, two integer ops on the chain.
 __device__ __forceinline__ double clip_mask(double v, int okm) {
 #ifndef NTF_NNLS_FCLIP
+  // arithmetic shift of the sign, then one 3-input LOP3 per word
+  // (x & ~(sign & okm), immLut 0x70): two dependent steps on the chain
   const int hi = __double2hiint(v), lo = __double2loint(v);
-  const int m = (hi >> 31) & okm;
-  return __hiloint2double(hi & ~m, lo & ~m);
+  int h2, l2;
+  asm("{\n\t.reg .b32 m;\n\tshr.s32 m, %2, 31;\n\tlop3.b32 %0, %2, m, %4, 0x70;\n\t"
+      "lop3.b32 %1, %3, m, %4, 0x70;\n\t}"
+      : "=r"(h2), "=r"(l2)
+      : "r"(hi), "r"(lo), "r"(okm));
+  return __hiloint2double(h2, l2);
 #else
   return (okm != 0 && v < 0.0) ? 0.0 : v;
 #endif

@@ -30,15 +30,18 @@ for name in sys.argv[1:] or ["c2"]:
     rng = np.random.default_rng(1)
     pert = [a * np.where(rng.random(a.shape) < 0.5, 1.0 + 2.0 ** -52, 1.0) for a in init]
     nsq = O.norm_sq(t)
-    for exp, algo in (("ulp", "her"), ("ulp", "ao"), ("order", "her"), ("order", "ao")):
-        O.set_sum_order(1 if exp == "order" else 0)
-        _, f0, recs = O.run(algo, t, pert if exp == "ulp" else init, max_outer_iters=50)
+    exps = [("ulp", "her"), ("ulp", "ao"), ("order", "her"), ("order", "ao")]
+    if dt == "f32":  # FP32 factor mirrors: Khatri-Rao rows rounded to float
+        exps += [("f32kr", "her"), ("f32kr", "ao")]
+    for exp, algo in exps:
+        O.set_sum_order({"order": 1, "f32kr": 2}.get(exp, 0))
+        fac_p, f0, recs = O.run(algo, t, pert if exp == "ulp" else init, max_outer_iters=50)
         O.set_sum_order(0)
         f = np.array([r["f"] for r in recs])
         ref = g[f"{algo}_f"]
         rel = np.abs(f - ref) / np.abs(ref)
         absn = np.abs(f - ref) / nsq
-        res = {"f0_rel": abs(f0 - float(g[f"{algo}_f0"])) / abs(float(g[f"{algo}_f0"])), "max_rel": float(rel.max()), "argmax": int(rel.argmax()) + 1, "max_abs_over_nsq": float(absn.max()),
+        res = {"e_rel": abs(O.factor_error(fac_p, truth) - float(g[f"{algo}_e"])) / float(g[f"{algo}_e"]), "f0_rel": abs(f0 - float(g[f"{algo}_f0"])) / abs(float(g[f"{algo}_f0"])), "max_rel": float(rel.max()), "argmax": int(rel.argmax()) + 1, "max_abs_over_nsq": float(absn.max()),
                "rel_at": {k: float(rel[k - 1]) for k in (1, 5, 10, 20, 30, 40, 50)}}
         if algo == "her":
             res["restart_flips"] = int(sum(bool(r["restarted"]) != bool(x) for r, x in zip(recs, g["her_restarted"])))
