@@ -53,7 +53,6 @@ using fast::mbar_init;
 using fast::mbar_wait;
 using fast::tma_load_3d;
 
-constexpr int kKB = 16;  // reduction indices per unit (one 128-byte box of doubles)
 
 // First unit of CTA b: W b / G, or (tall views, align) the first unit of
 // tile n_tiles b / G -- the host tables (sk_choose) use the same formula.
@@ -61,10 +60,159 @@ __host__ __device__ __forceinline__ long long range_lo(const SkParams& p, int G,
   return p.align ? p.U * ((long long)p.n_tiles * b / G) : p.W * b / G;
 }
 
-template <int NMF, int NNF, int LAYOUT>
+__device__ __forceinline__ float2 ffma2(float a, float2 b, float2 c) {
+  // packed FP32 FMA (SASS FFMA2, scalar a broadcast to both lanes)
+  unsigned long long d;
+  const float2 aa = make_float2(a, a);
+  asm("fma.rn.f32x2 %0, %1, %2, %3;"
+      : "=l"(d)
+      : "l"(*reinterpret_cast<const unsigned long long*>(&aa)), "l"(*reinterpret_cast<const unsigned long long*>(&b)),
+        "l"(*reinterpret_cast<const unsigned long long*>(&c)));
+  return *reinterpret_cast<float2*>(&d);
+}
+
+// FP32 consumer warp of the stream-K kernel: lane (rg, cg) owns 8 rows x 8
+// columns (columns cg*8.., rows rg + RG*i for ROW views, groups of four
+// consecutive rows for COL views) as 32 float2 accumulators fed by packed
+// FFMA2 -- 64 FMAs per 4-8 shared loads (T values are 16-byte reads of
+// four k of a row (ROW) or four rows of a k (COL); W values 16-byte
+// broadcast reads). Every p.flush_units units and at a tile segment's end
+// the FP32 sums are added into FP64 (each lane its own entries: no race),
+// so no FP32 sum runs over more than flush_units * 32 terms (the FP32 bar of
+// BASELINE configs 4/5, mttkrp_fast_impl.cuh).
+template <int CG, int LAYOUT>
+__device__ __forceinline__ void consume_f32(const SkParams& p, const unsigned char* t_base, const unsigned char* w_base,
+                                            const unsigned char* aq_base, uint64_t* full, uint64_t* empty, long long w0,
+                                            long long w1, long long U, const int* tile_ctas, int b, int cw, int lane) {
+  constexpr int RG = 32 / CG, A = 8, RW = RG * A, KB = 32;
+  const int r = p.v.rank;
+  const int rg = lane % RG, cg = lane / RG;
+  auto lrow = [&](int i) {
+    return LAYOUT == fast::kRow ? cw * RW + rg + RG * i : cw * RW + 4 * rg + 4 * RG * (i >> 2) + (i & 3);
+  };
+  float2 acc[A][4];
+#pragma unroll
+  for (int i = 0; i < A; ++i)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc[i][q] = make_float2(0.f, 0.f);
+  // ROW: the byte offset of each row and its swizzle key; COL: the two
+  // 4-row groups' element offsets
+  int roff[A];
+#pragma unroll
+  for (int i = 0; i < A; ++i) {
+    const int m = lrow(i);
+    roff[i] = LAYOUT == fast::kRow ? m * 128 : ((m / p.m_box) * p.m_pitch * KB + (m % p.m_box)) * 4;
+  }
+  const unsigned bpitch = p.direct_b ? unsigned(r) * 4u : unsigned(p.wld) * 4u;
+  const int wcol = cg * 32;  // bytes: columns cg*8 .. cg*8+7
+  const unsigned tpitch = unsigned(p.m_pitch) * 4u;
+  int s = 0;
+  uint32_t phase = 0;
+  const int first_tile = int(w0 / U);
+  int tile = first_tile;
+  long long u_in = w0 - (long long)first_tile * U;
+  int since = 0;
+  bool started = false;  // the segment's FP64 target holds a first flush
+  auto flush = [&](bool seg_end) {
+    const int2 cs = reinterpret_cast<const int2*>(tile_ctas)[tile];
+    const bool direct = cs.x == cs.y;
+    double* dst = direct ? p.out : p.partial + size_t(2 * b + (tile == first_tile ? 0 : 1)) * p.m_cta * r;
+    const long long row0 = direct ? (long long)tile * p.m_cta : 0;
+#pragma unroll
+    for (int i = 0; i < A; ++i) {
+      const int m = lrow(i);
+      if ((long long)tile * p.m_cta + m >= p.v.I) continue;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int c = cg * 8 + 2 * q;
+        if (c < r) {
+          double2* d = reinterpret_cast<double2*>(dst + (row0 + m) * r + c);
+          double2 v = make_double2(double(acc[i][q].x), double(acc[i][q].y));
+          if (started) {
+            const double2 o = *d;
+            v.x += o.x;
+            v.y += o.y;
+          }
+          *d = v;
+        }
+        acc[i][q] = make_float2(0.f, 0.f);
+      }
+    }
+    started = !seg_end;
+    since = 0;
+  };
+  for (long long w = w0; w < w1; ++w) {
+    mbar_wait(&full[s], phase);
+    const unsigned char* ts = t_base + size_t(s) * p.t_stage_bytes;
+    const unsigned char* wsb = p.direct_b ? aq_base + size_t(s) * p.aq_stage_bytes : w_base + size_t(s) * p.w_stage_bytes;
+    if (LAYOUT == fast::kRow) {
+#pragma unroll 2
+      for (int kq = 0; kq < KB / 4; ++kq) {
+        float4 t[A];
+#pragma unroll
+        for (int i = 0; i < A; ++i) {
+          const int key = (roff[i] >> 7) & 7;
+          t[i] = *reinterpret_cast<const float4*>(ts + roff[i] + (((kq ^ key) & 7) << 4));
+        }
+        float2 wv[4][4];
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+          const float4 a = *reinterpret_cast<const float4*>(wsb + (4 * kq + kk) * bpitch + wcol);
+          const float4 c = *reinterpret_cast<const float4*>(wsb + (4 * kq + kk) * bpitch + wcol + 16);
+          wv[kk][0] = make_float2(a.x, a.y);
+          wv[kk][1] = make_float2(a.z, a.w);
+          wv[kk][2] = make_float2(c.x, c.y);
+          wv[kk][3] = make_float2(c.z, c.w);
+        }
+#pragma unroll
+        for (int i = 0; i < A; ++i) {
+          const float tk[4] = {t[i].x, t[i].y, t[i].z, t[i].w};
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) acc[i][q] = ffma2(tk[kk], wv[kk][q], acc[i][q]);
+        }
+      }
+    } else {
+#pragma unroll 4
+      for (int k = 0; k < KB; ++k) {
+        const float4 ta = *reinterpret_cast<const float4*>(ts + roff[0] + k * tpitch);
+        const float4 tb = *reinterpret_cast<const float4*>(ts + roff[4] + k * tpitch);
+        const float4 a = *reinterpret_cast<const float4*>(wsb + k * bpitch + wcol);
+        const float4 c = *reinterpret_cast<const float4*>(wsb + k * bpitch + wcol + 16);
+        const float2 wv[4] = {make_float2(a.x, a.y), make_float2(a.z, a.w), make_float2(c.x, c.y),
+                              make_float2(c.z, c.w)};
+        const float tv[A] = {ta.x, ta.y, ta.z, ta.w, tb.x, tb.y, tb.z, tb.w};
+#pragma unroll
+        for (int i = 0; i < A; ++i)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) acc[i][q] = ffma2(tv[i], wv[q], acc[i][q]);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+    if (++s == p.stages) {
+      s = 0;
+      phase ^= 1;
+    }
+    const bool seg_end = ++u_in == U || w + 1 == w1;
+    if (seg_end || (p.flush_units > 0 && ++since == p.flush_units)) flush(seg_end);
+    if (seg_end) {
+      u_in = 0;
+      ++tile;
+    }
+  }
+}
+
+// T = double: DMMA consumers, NMF 8-row fragments x NNF 8-column fragments
+// per warp. T = float (FP32 tensors, FP32 factor mirrors): FFMA2 register
+// tiles of 8 rows x 8 columns per lane, NNF = column groups of 8 (RG = 32 /
+// NNF row groups), FP32 sums flushed into FP64 every p.flush_units units.
+template <typename T, int NMF, int NNF, int LAYOUT>
 __global__ void __launch_bounds__(32 * (kMaxNP + kMaxMW), 1) mttkrp_sk_kernel(const __grid_constant__ CUtensorMap tmap,
                                                                             SkParams p) {
-  constexpr int RW = 8 * NMF;  // rows per consumer warp
+  constexpr int KBT = 128 / int(sizeof(T));  // reduction indices per unit
+  constexpr int RW = sizeof(T) == 8 ? 8 * NMF : (32 / NNF) * 8;  // rows per consumer warp
   extern __shared__ __align__(1024) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const ModeView& v = p.v;
@@ -74,8 +222,8 @@ __global__ void __launch_bounds__(32 * (kMaxNP + kMaxMW), 1) mttkrp_sk_kernel(co
   // slots (aq) | barriers. direct_b (no base modes): the B operand is the
   // factor rows themselves, one aq slot per stage, no W stage.
   unsigned char* t_base = smem;
-  double* w_base = reinterpret_cast<double*>(smem + size_t(stages) * p.t_stage_bytes);
-  double* aq_base = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(w_base) + size_t(stages) * p.w_stage_bytes);
+  T* w_base = reinterpret_cast<T*>(smem + size_t(stages) * p.t_stage_bytes);
+  T* aq_base = reinterpret_cast<T*>(reinterpret_cast<unsigned char*>(w_base) + size_t(stages) * p.w_stage_bytes);
   const int n_aq = p.direct_b ? stages : p.NP * p.naw;
   uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(aq_base) + size_t(n_aq) * p.aq_stage_bytes);
   uint64_t* empty = full + stages;
@@ -102,8 +250,8 @@ __global__ void __launch_bounds__(32 * (kMaxNP + kMaxMW), 1) mttkrp_sk_kernel(co
   // slots too, so B rows past a unit's valid k are finite (they multiply the
   // zero-filled T rows)
   {
-    const int nw = (stages * int(p.w_stage_bytes) + n_aq * int(p.aq_stage_bytes)) / 8;
-    for (int e = threadIdx.x; e < nw; e += blockDim.x) w_base[e] = 0.0;
+    const int nw = (stages * int(p.w_stage_bytes) + n_aq * int(p.aq_stage_bytes)) / int(sizeof(T));
+    for (int e = threadIdx.x; e < nw; e += blockDim.x) w_base[e] = T(0);
   }
   __syncthreads();
 
@@ -116,13 +264,13 @@ __global__ void __launch_bounds__(32 * (kMaxNP + kMaxMW), 1) mttkrp_sk_kernel(co
     // unit's stage is free (TMA issued) its rows have landed and W is formed
     // at once. direct_b: one bulk copy per unit into the stage's aq slot,
     // completing on the stage's full barrier with the TMA box.
-    constexpr int KB = kKB;
-    const double* fL = factor_ptr<double>(p.F, p.qL);
-    const double* bfac[kMaxBase];
+    constexpr int KB = KBT;
+    const T* fL = factor_ptr<T>(p.F, p.qL);
+    const T* bfac[kMaxBase];
 #pragma unroll
-    for (int t = 0; t < kMaxBase; ++t) bfac[t] = t < p.nb ? factor_ptr<double>(p.F, p.bq[t]) : nullptr;
-    const unsigned row_bytes = unsigned(r * sizeof(double));
-    const int aq_elems = int(p.aq_stage_bytes / sizeof(double));
+    for (int t = 0; t < kMaxBase; ++t) bfac[t] = t < p.nb ? factor_ptr<T>(p.F, p.bq[t]) : nullptr;
+    const unsigned row_bytes = unsigned(r * sizeof(T));
+    const int aq_elems = int(p.aq_stage_bytes / sizeof(T));
     auto aq_of = [&](int q) { return aq_base + size_t(q) * aq_elems; };
     auto info_of = [&](int q) { return reinterpret_cast<int*>(aq_of(q) + (KB + 2 * kMaxBase) * r); };
     const long long n_units = w1 - w0;
@@ -164,7 +312,7 @@ __global__ void __launch_bounds__(32 * (kMaxNP + kMaxMW), 1) mttkrp_sk_kernel(co
     // earlier by this lane) instead of a second global round trip
     auto copy_rows = [&](const int (&e)[kUnitInts], int q, uint64_t* bar, bool arm) {
       const int n_valid = e[3], n1 = e[4], kwrap = e[5];
-      double* aq = aq_of(q);
+      T* aq = aq_of(q);
       int* info = info_of(q);
 #pragma unroll
       for (int i = 0; i < kUnitInts; ++i) info[i] = e[i];
@@ -188,10 +336,10 @@ __global__ void __launch_bounds__(32 * (kMaxNP + kMaxMW), 1) mttkrp_sk_kernel(co
         if (LAYOUT == fast::kRow)
           tma_load_3d(ts + size_t(mb) * p.m_box * 128, &tmap, &full[s], e[0], m0, e[1]);
         else
-          tma_load_3d(ts + size_t(mb) * p.m_pitch * KB * sizeof(double), &tmap, &full[s], m0, e[0], 0);
+          tma_load_3d(ts + size_t(mb) * p.m_pitch * KB * sizeof(T), &tmap, &full[s], m0, e[0], 0);
       }
     };
-    constexpr int CPL = (8 * NNF + 31) / 32;  // columns per lane
+    const int CPL = (r + 31) / 32;  // columns per lane
     int s = warp;
     uint32_t round = 0;
     Cursor cur = cursor_at(0), ahead = cursor_at(DA);
@@ -248,17 +396,16 @@ __global__ void __launch_bounds__(32 * (kMaxNP + kMaxMW), 1) mttkrp_sk_kernel(co
           ++aq_round;
         }
         mbar_wait(&aqb[q], ph);
-        double* ws = w_base + size_t(s) * (p.w_stage_bytes / sizeof(double));
-        const double* aq = aq_of(q);
+        T* ws = w_base + size_t(s) * (p.w_stage_bytes / sizeof(T));
+        const T* aq = aq_of(q);
         const int* info = info_of(q);
         const int kmax = info[3];
         const int kwrap = info[5];
         const bool wrap = kwrap < KB;
-#pragma unroll
         for (int ci = 0; ci < CPL; ++ci) {
           const int c = lane + 32 * ci;
           if (c >= r) continue;
-          double base0 = 1.0, base1 = 1.0;
+          T base0 = T(1), base1 = T(1);
 #pragma unroll
           for (int t = 0; t < kMaxBase; ++t)
             if (t < p.nb) {
@@ -267,7 +414,7 @@ __global__ void __launch_bounds__(32 * (kMaxNP + kMaxMW), 1) mttkrp_sk_kernel(co
             }
 #pragma unroll
           for (int k = 0; k < KB; ++k)
-            ws[k * p.wld + c] = (k < kmax) ? (k >= kwrap ? base1 : base0) * aq[k * r + c] : 0.0;
+            ws[k * p.wld + c] = (k < kmax) ? (k >= kwrap ? base1 : base0) * aq[k * r + c] : T(0);
         }
         mbar_arrive(&full[s]);
       }
@@ -278,6 +425,11 @@ __global__ void __launch_bounds__(32 * (kMaxNP + kMaxMW), 1) mttkrp_sk_kernel(co
     }
   } else if (warp < NP + MW) {
     // ------------------------------------------------------------ consumers
+    if constexpr (sizeof(T) == 4) {
+      consume_f32<NNF, LAYOUT>(p, t_base, reinterpret_cast<const unsigned char*>(w_base),
+                               reinterpret_cast<const unsigned char*>(aq_base), full, empty, w0, w1, U,
+                               tile_ctas, b, warp - NP, lane);
+    } else {
     const int cw = warp - NP;
     const int g8 = lane >> 2, t4 = lane & 3;
     // ROW fragments take rows with swizzle keys 0,2,4,6 | 1,3,5,7 on the two
@@ -292,7 +444,7 @@ __global__ void __launch_bounds__(32 * (kMaxNP + kMaxMW), 1) mttkrp_sk_kernel(co
     for (int f = 0; f < NMF; ++f) {
       const int m = cw * RW + 8 * f + frow;
       moff[f] = LAYOUT == fast::kRow ? (cw * RW + frow) * 128 + f * 1024
-                                     : ((m / p.m_box) * p.m_pitch * kKB + (m % p.m_box)) * 8;
+                                     : ((m / p.m_box) * p.m_pitch * KBT + (m % p.m_box)) * 8;
     }
     const int wcol = g8 * 8;  // byte offset of column 8 jn + g8 within a W row (+ jn * 64)
     double acc[NMF][NNF][2];
@@ -385,6 +537,7 @@ __global__ void __launch_bounds__(32 * (kMaxNP + kMaxMW), 1) mttkrp_sk_kernel(co
         ++tile;
       }
     }
+    }  // DMMA consumer
   }
   if (!p.n_split) return;
   // ---------------------------------------------------- split-tile reduction
@@ -456,9 +609,9 @@ __global__ void __launch_bounds__(32 * (kMaxNP + kMaxMW), 1) mttkrp_sk_kernel(co
   }
 }
 
-template <int NMF, int NNF, int LAYOUT>
+template <typename T, int NMF, int NNF, int LAYOUT>
 void launch_sk(const CUtensorMap& map, const SkParams& p, int grid, int threads, size_t smem, cudaStream_t s) {
-  auto fn = mttkrp_sk_kernel<NMF, NNF, LAYOUT>;
+  auto fn = mttkrp_sk_kernel<T, NMF, NNF, LAYOUT>;
   NTF_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(unsigned(grid));
@@ -479,7 +632,16 @@ using SkLaunch = void (*)(const CUtensorMap&, const SkParams&, int, int, size_t,
 
 template <int NMF, int NNF>
 SkLaunch pick_layout(int layout) {
-  return layout == fast::kRow ? launch_sk<NMF, NNF, fast::kRow> : launch_sk<NMF, NNF, fast::kCol>;
+  return layout == fast::kRow ? launch_sk<double, NMF, NNF, fast::kRow> : launch_sk<double, NMF, NNF, fast::kCol>;
+}
+
+// FP32: NNF = column groups of 8 (4: r <= 32, 8: r <= 64)
+SkLaunch pick_f32(int cg, int layout) {
+  switch (cg) {
+    case 4: return layout == fast::kRow ? launch_sk<float, 1, 4, fast::kRow> : launch_sk<float, 1, 4, fast::kCol>;
+    case 8: return layout == fast::kRow ? launch_sk<float, 1, 8, fast::kRow> : launch_sk<float, 1, 8, fast::kCol>;
+    default: return nullptr;
+  }
 }
 
 template <int NMF>
@@ -527,25 +689,34 @@ constexpr size_t kSkSmem = 222 * 1024;  // of the 227 KB a CTA may claim
 }  // namespace
 
 bool sk_choose(const ModeView& v, int dtype, int sms, SkPlan* out) {
-  if (dtype != NTF_DTYPE_F64) return false;
   if (const char* e = std::getenv("NTF_SK"); e && std::atoi(e) == 0) return false;
+  const bool f32 = dtype == NTF_DTYPE_F32;
+  if (f32 && std::getenv("NTF_SK_F32") && std::atoi(std::getenv("NTF_SK_F32")) == 0) return false;
+  const int es = f32 ? 4 : 8;
+  const int KB = 128 / es;
   const int r = v.rank;
-  if (r % 2 || r > 32) return false;
-  const int nnf = (r + 7) / 8;
+  int nnf;
+  if (f32) {  // FFMA2 tiles of 8 x 8 per lane: column groups of 8
+    if (r <= 16 || r > 64 || (r * 4) % 16) return false;
+    nnf = r <= 32 ? 4 : 8;
+  } else {
+    if (r % 2 || r > 32) return false;
+    nnf = (r + 7) / 8;
+  }
   if (v.L * v.I * v.R < (1LL << 15)) return false;
   if (v.L >= (1LL << 31) || v.R >= (1LL << 31)) return false;
   int layout;
   if (v.R > 1) {
     layout = fast::kRow;
-    if ((v.R * 8) % 16 || (v.I * v.R * 8) % 16) return false;
+    if ((v.R * es) % 16 || (v.I * v.R * es) % 16) return false;
   } else if (v.L > 1) {
     layout = fast::kCol;
-    if ((v.I * 8) % 16) return false;
+    if ((v.I * es) % 16) return false;
   } else {
     return false;
   }
   const int qL = layout == fast::kRow ? v.order - 1 : v.order - 2;
-  if (v.dims[qL] < sk::kKB) return false;
+  if (v.dims[qL] < KB) return false;
   if (v.order > fast::kMaxBase + 2) return false;
   // tile: four consumer warps (one per SM sub-partition) of NMF fragments;
   // a short mode gets one tile of ten-fragment warps (C2: 300 rows -> 320)
@@ -575,8 +746,14 @@ bool sk_choose(const ModeView& v, int dtype, int sms, SkPlan* out) {
     align = 1;
   }
   if (const char* e = std::getenv("NTF_SK_NMF")) nmf = std::atoi(e);
+  if (f32) {  // four warps of (32 / nnf) x 8 rows: 256 (r <= 32) or 128 (r <= 64) row tiles
+    mw = 4;
+    nmf = 1;
+    align = 0;
+  }
   if (const char* e = std::getenv("NTF_SK_ALIGN")) align = std::atoi(e);
-  const int m_cta = rows_per_frag_set * nmf;
+  const int m_cta = f32 ? 4 * (32 / nnf) * 8 : rows_per_frag_set * nmf;
+  if (f32 && (v.I + m_cta - 1) / m_cta >= 4LL * sms && !std::getenv("NTF_SK_ALIGN")) align = 1;
   SkPlan pl;
   SkParams& p = pl.p;
   p = SkParams{};
@@ -590,13 +767,13 @@ bool sk_choose(const ModeView& v, int dtype, int sms, SkPlan* out) {
   if (p.m_box * p.n_mbox != m_cta || p.m_box % 8) return false;
   p.wld = 8 * nnf + 4;  // 32 B off the 64-byte bank period (4 k rows per half-warp)
   if (layout == fast::kRow) {
-    p.U = v.L * ((v.R + sk::kKB - 1) / sk::kKB);  // (l, rho box) units, as the unit table
+    p.U = v.L * ((v.R + KB - 1) / KB);  // (l, rho box) units, as the unit table
     p.m_pitch = p.m_box;
     p.t_stage_bytes = unsigned(m_cta * 128);
   } else {
-    p.U = (v.L + sk::kKB - 1) / sk::kKB;
-    p.m_pitch = p.m_box + 4 <= 256 ? p.m_box + 4 : p.m_box;
-    p.t_stage_bytes = unsigned(size_t(p.n_mbox) * p.m_pitch * sk::kKB * 8);
+    p.U = (v.L + KB - 1) / KB;
+    p.m_pitch = !f32 && p.m_box + 4 <= 256 ? p.m_box + 4 : p.m_box;
+    p.t_stage_bytes = unsigned(size_t(p.n_mbox) * p.m_pitch * KB * es);
   }
   p.n_tiles = int((v.I + m_cta - 1) / m_cta);
   p.W = (long long)p.n_tiles * p.U;
@@ -620,9 +797,11 @@ bool sk_choose(const ModeView& v, int dtype, int sms, SkPlan* out) {
   }
   // aq slots per producer warp (copies run naw - 1 of its units ahead): 4,
   // fewer when the T stages would drop below four (C2's 300-row COL view)
-  p.w_stage_bytes = p.direct_b ? 0u : unsigned((size_t(sk::kKB) * p.wld * 8 + 127) / 128 * 128);
-  p.aq_stage_bytes = unsigned(((size_t(sk::kKB) + 2 * fast::kMaxBase) * r * 8 + fast::kUnitInts * sizeof(int) + 127) /
+  p.w_stage_bytes = p.direct_b ? 0u : unsigned((size_t(KB) * p.wld * es + 127) / 128 * 128);
+  p.aq_stage_bytes = unsigned(((size_t(KB) + 2 * fast::kMaxBase) * r * es + fast::kUnitInts * sizeof(int) + 127) /
                               128 * 128);
+  // FP32: no FP32 register sum over more than 16384 terms (512 units of 32)
+  p.flush_units = f32 ? 16384 / KB : 0;
   const size_t per_stage = size_t(p.t_stage_bytes) + p.w_stage_bytes + (p.direct_b ? p.aq_stage_bytes : 0u);
   size_t fixed = 0;
   for (p.naw = 4; p.naw >= 2; --p.naw) {
@@ -643,7 +822,8 @@ bool sk_choose(const ModeView& v, int dtype, int sms, SkPlan* out) {
   pl.layout = layout;
   pl.nmf = nmf;
   pl.nnf = nnf;
-  if (!sk::pick(nmf, nnf, layout)) return false;
+  pl.f32 = f32;
+  if (!(f32 ? sk::pick_f32(nnf, layout) : sk::pick(nmf, nnf, layout))) return false;
   // contributors per tile and the split tiles
   pl.tile_ctas.assign(size_t(2 * p.n_tiles), 0);
   for (int t = 0; t < p.n_tiles; ++t) {
@@ -690,13 +870,15 @@ void sk_mttkrp(const void* t, const ModeView& v, const SkPlan& pl, const DevFact
   cuuint64_t dims[3], strides[2];
   cuuint32_t box[3], estr[3] = {1, 1, 1};
   CUtensorMapSwizzle sw;
+  const size_t es = pl.f32 ? 4 : 8;
+  const cuuint32_t KB = cuuint32_t(128 / es);
   if (pl.layout == fast::kRow) {
     dims[0] = cuuint64_t(v.R);
     dims[1] = cuuint64_t(v.I);
     dims[2] = cuuint64_t(v.L);
-    strides[0] = cuuint64_t(v.R * 8);
-    strides[1] = cuuint64_t(v.I * v.R * 8);
-    box[0] = sk::kKB;
+    strides[0] = cuuint64_t(v.R * es);
+    strides[1] = cuuint64_t(v.I * v.R * es);
+    box[0] = KB;
     box[1] = cuuint32_t(p0.m_box);
     box[2] = 1;
     sw = CU_TENSOR_MAP_SWIZZLE_128B;
@@ -704,14 +886,15 @@ void sk_mttkrp(const void* t, const ModeView& v, const SkPlan& pl, const DevFact
     dims[0] = cuuint64_t(v.I);
     dims[1] = cuuint64_t(v.L);
     dims[2] = 1;
-    strides[0] = cuuint64_t(v.I * 8);
-    strides[1] = cuuint64_t(v.I * v.L * 8);
+    strides[0] = cuuint64_t(v.I * es);
+    strides[1] = cuuint64_t(v.I * v.L * es);
     box[0] = cuuint32_t(p0.m_pitch);
-    box[1] = sk::kKB;
+    box[1] = KB;
     box[2] = 1;
     sw = CU_TENSOR_MAP_SWIZZLE_NONE;
   }
-  const CUresult rr = fn(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<void*>(t), dims, strides, box, estr,
+  const CUresult rr = fn(&map, pl.f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3,
+                         const_cast<void*>(t), dims, strides, box, estr,
                          CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (rr != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed (" + std::to_string(int(rr)) + ")");
@@ -727,15 +910,18 @@ void sk_mttkrp(const void* t, const ModeView& v, const SkPlan& pl, const DevFact
   p.rowL_wrap = modes.rowL_wrap;
   p.pdl = pdl && !p.n_split ? 1 : 0;  // (a cooperative split-tile launch is never a dependent)
   if (p.n_split && !counter) throw LogicError("stream-K MTTKRP needs an arrival counter");
-  sk::pick(pl.nmf, pl.nnf, pl.layout)(map, p, pl.grid, pl.threads, pl.smem, s);
+  (pl.f32 ? sk::pick_f32(pl.nnf, pl.layout) : sk::pick(pl.nmf, pl.nnf, pl.layout))(map, p, pl.grid, pl.threads, pl.smem,
+                                                                                   s);
 }
 
 std::string sk_describe(const SkPlan& pl) {
   char buf[256];
-  snprintf(buf, sizeof buf, "sk-%s+dmma NMF=%d NNF=%d MW=%d NP=%d m_cta=%d stages=%d grid=%d threads=%d smem=%zu "
+  snprintf(buf, sizeof buf,
+           "sk-%s+%s NMF=%d NNF=%d MW=%d NP=%d m_cta=%d stages=%d grid=%d threads=%d smem=%zu "
            "tiles=%d units/tile=%lld split=%d align=%d lpo=%d direct_b=%d naw=%d",
-           pl.layout == fast::kRow ? "row" : "col", pl.nmf, pl.nnf, pl.p.MW, pl.p.NP, pl.p.m_cta, pl.p.stages, pl.grid,
-           pl.threads, pl.smem, pl.p.n_tiles, pl.p.U, pl.p.n_split, pl.p.align, pl.p.lpo, pl.p.direct_b, pl.p.naw);
+           pl.layout == fast::kRow ? "row" : "col", pl.f32 ? "ffma2" : "dmma", pl.nmf, pl.nnf, pl.p.MW, pl.p.NP,
+           pl.p.m_cta, pl.p.stages, pl.grid, pl.threads, pl.smem, pl.p.n_tiles, pl.p.U, pl.p.n_split, pl.p.align,
+           pl.p.lpo, pl.p.direct_b, pl.p.naw);
   return buf;
 }
 

@@ -27,6 +27,7 @@ struct SkParams {
   int lpo;    // split-tile reduction: lanes per output (1, or 8 for wide fan-in)
   int direct_b;  // no base modes: DMMA B operand = the bulk-copied factor rows (no W formation)
   int naw;       // W formation: aq slots per producer warp
+  int flush_units;  // FP32: FP64 flush every flush_units units (0: at segment ends only)
   int pdl;       // host only: launch as a programmatic dependent
   int m_box, n_mbox, m_cta, m_pitch;
   int MW, NP, stages, wld;
@@ -37,6 +38,7 @@ struct SkParams {
 struct SkPlan {
   SkParams p{};
   int grid = 0, threads = 0, layout = 0, nmf = 0, nnf = 0;
+  bool f32 = false;
   size_t smem = 0;
   std::vector<int> tile_ctas;  // [n_tiles][2]: first / last CTA touching the tile
   std::vector<int> split;      // tiles with more than one contributor
