@@ -839,8 +839,6 @@ __global__ void __launch_bounds__(kStreamTPB, 1) nnls_stream_kernel(NnlsLaunch a
       if (e < nloc * RP) Cs[(e / RP) * LDC + e % RP] = cv[u];
     }
   };
-  double cv0[4];
-  load_c(int(threadIdx.x), cv0);
   const long long t_q0 = clock64();
   // ---- G: Hadamard of the other modes' Grams (kernels.cpp:193-200).
   // (global loads of four entries per thread in flight together)
@@ -871,13 +869,7 @@ __global__ void __launch_bounds__(kStreamTPB, 1) nnls_stream_kernel(NnlsLaunch a
     }
   }
   const long long t_q1 = clock64();
-  store_c(int(threadIdx.x), cv0);
   const long long t_q2 = clock64();
-  for (int e0 = int(threadIdx.x) + 4 * int(blockDim.x); e0 < nloc * RP; e0 += 4 * int(blockDim.x)) {
-    double cv[4];
-    load_c(e0, cv);
-    store_c(e0, cv);
-  }
   if (threadIdx.x == 0) {
     for (int b = 0; b < D; ++b)
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&rowbar[b])) : "memory");
@@ -917,6 +909,16 @@ __global__ void __launch_bounds__(kStreamTPB, 1) nnls_stream_kernel(NnlsLaunch a
       if (d <= L - 1 && j < r && c < r && ((okbits >> c) & 1)) h = Gs[j * RP + c] * Ginv[c];
       wn[e] = h;
     }
+  }
+  // Everything above depends only on earlier blocks (Grams, roles) and runs
+  // while the kernel producing C (the block's MTTKRP contraction, of which
+  // this kernel is a programmatic dependent) finishes: wait for it now,
+  // then the C rows (and, with another inner solver, its result rows w0).
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  for (int e0 = int(threadIdx.x); e0 < nloc * RP; e0 += 4 * int(blockDim.x)) {
+    double cv[4];
+    load_c(e0, cv);
+    store_c(e0, cv);
   }
   const long long t_p2 = clock64();
   cl.sync();  // tables, C rows and every CTA's mbarriers exist before any st.async targets them
@@ -1428,13 +1430,17 @@ bool launch_stream_q(const NnlsLaunch& a, cudaStream_t s) {
   cfg.blockDim = dim3(threads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = cl;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  // drivers: a programmatic dependent of the block's MTTKRP kernel (the
+  // prologue overlaps it; griddepcontrol.wait before the C rows)
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = (a.role != 2 && !std::getenv("NTF_NNLS_NO_PDL")) ? 1 : 0;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   NTF_CUDA(cudaLaunchKernelExC(&cfg, reinterpret_cast<const void*>(fn), params));
   return true;
 }

@@ -192,6 +192,9 @@ template <int R_MAX>
 __global__ void __launch_bounds__(256) tree2_kernel(const double* __restrict__ Y, TreeView v,
                                                     const DevFactors* __restrict__ F, double* __restrict__ out) {
   __shared__ double fold[256];
+  // the block's NNLS (a programmatic dependent) may launch and run its
+  // prologue now; it waits for this grid before reading the result
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int r = v.rank;
   const int i = int(blockIdx.x);
   const int G = int(blockDim.x) / r;
