@@ -209,7 +209,10 @@ CallCache& call_setup(ntf_ctx* ctx, const ntf_tensor* t, const double* factors, 
     c = std::move(n);
   }
   NTF_CUDA(cudaMemcpyAsync(c->fac.p, factors, c->fac.bytes, cudaMemcpyHostToDevice, ctx->stream));
-  launch_init_factors(c->dF.as<DevFactors>(), c->h, ctx->stream);
+  if (c->gscratch.bytes < init_factors_scratch(c->h) * sizeof(double))
+    c->gscratch = DevBuf(init_factors_scratch(c->h) * sizeof(double));
+  launch_init_factors(c->dF.as<DevFactors>(), c->h, c->gscratch.as<double>(), c->gscratch.bytes / sizeof(double),
+                      ctx->stream);
   return *c;
 }
 
@@ -705,9 +708,9 @@ int ntf_mttkrp_all(ntf_ctx* ctx, const ntf_tensor* t, const double* factors, int
     need(ctx, "ctx");
     need(t, "tensor");
     need(out, "out");
-    if (flags & ~(NTF_RUN_DIMTREE | NTF_RUN_DIRECT | NTF_RUN_GENERIC | NTF_RUN_NO_GRAPH))
+    if (flags & ~(NTF_RUN_DIMTREE | NTF_RUN_DIRECT | NTF_RUN_GENERIC | NTF_RUN_NO_GRAPH | NTF_RUN_NO_OVERLAP))
       throw InvalidArgument("unknown NTF_RUN_* flags");
-    CallCache& c = call_setup(ctx, t, factors, rank, flags & (NTF_RUN_DIRECT | NTF_RUN_GENERIC));
+    CallCache& c = call_setup(ctx, t, factors, rank, flags & (NTF_RUN_DIRECT | NTF_RUN_GENERIC | NTF_RUN_NO_OVERLAP));
     long long off = 0;
     for (int m = 0; m < t->order; ++m) {  // sweep order: the tree forms Y_L at block 0, Y_R at block h
       c.eng->run(m, c.dF.as<DevFactors>(), c.C.as<double>(), ctx->stream);

@@ -150,42 +150,6 @@ __global__ void sum_scratch_kernel(const double* __restrict__ scratch, int n, do
 }
 
 // Gram of one row-major rows x r matrix, ascending-row order per entry.
-// g = a^T a over `rows` rows (one CTA). Thread t owns Gram entry t % r^2 of
-// row group t / r^2 (groups = blockDim / r^2 when r^2 <= blockDim) and keeps
-// four independent partial sums over its rows (no serial add chain); the
-// groups are folded in group order through `red` (>= blockDim doubles), so
-// the result is deterministic.
-__device__ void gram_rows(const double* __restrict__ a, int rows, int r, double* __restrict__ g,
-                          double* __restrict__ red) {
-  const int rr = r * r;
-  const int groups = rr <= int(blockDim.x) ? int(blockDim.x) / rr : 1;
-  for (int base = 0; base < rr; base += int(blockDim.x) / groups * 1) {
-    const int e = base + int(threadIdx.x) % (int(blockDim.x) / groups);
-    const int grp = int(threadIdx.x) / (int(blockDim.x) / groups);
-    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-    if (e < rr && grp < groups) {
-      const int p = e / r, q = e % r;
-      int i = grp;
-      for (; i + 3 * groups < rows; i += 4 * groups) {
-        s0 += a[(long long)i * r + p] * a[(long long)i * r + q];
-        s1 += a[(long long)(i + groups) * r + p] * a[(long long)(i + groups) * r + q];
-        s2 += a[(long long)(i + 2 * groups) * r + p] * a[(long long)(i + 2 * groups) * r + q];
-        s3 += a[(long long)(i + 3 * groups) * r + p] * a[(long long)(i + 3 * groups) * r + q];
-      }
-      for (; i < rows; i += groups) s0 += a[(long long)i * r + p] * a[(long long)i * r + q];
-    }
-    red[threadIdx.x] = (s0 + s1) + (s2 + s3);
-    __syncthreads();
-    const int span = int(blockDim.x) / groups;
-    if (int(threadIdx.x) < span && base + int(threadIdx.x) < rr) {
-      double t = 0.0;
-      for (int k = 0; k < groups; ++k) t += red[k * span + threadIdx.x];
-      g[base + threadIdx.x] = t;
-    }
-    __syncthreads();
-  }
-}
-
 // Fixed-order block sum of one value per thread (blockDim a power of two).
 __device__ double block_sum(double v, double* __restrict__ red) {
   red[threadIdx.x] = v;
@@ -200,34 +164,67 @@ __device__ double block_sum(double v, double* __restrict__ red) {
 }
 
 constexpr int kSetupThreads = 1024;
+constexpr int kGramThreads = 256;
+constexpr int kGramRows = 32;  // rows per partial-Gram CTA
 
-// Grams of the X-role buffers plus the FP32 mirrors of both buffers; one CTA
-// per mode.
-__global__ void __launch_bounds__(kSetupThreads) init_factors_kernel(DevFactors* F) {
-  __shared__ double red[kSetupThreads];
-  const int mode = blockIdx.x;
+// Partial Grams of the X-role buffers: CTA (mode, chunk) sums its rows'
+// outer products (thread e: entries e, e + 256, ...; rows in ascending
+// order), one slot per chunk; gram_finish adds the slots in chunk order.
+__global__ void __launch_bounds__(kGramThreads) gram_partial_kernel(const DevFactors* __restrict__ F,
+                                                                    double* __restrict__ part, int chunks) {
+  const int mode = blockIdx.x, chunk = blockIdx.y;
   const int rows = F->rows[mode], r = F->rank;
-  const int b = F->sel[mode];
-  gram_rows(F->x[mode][b], rows, r, F->gram[mode][b], red);
+  const int rpc = (rows + chunks - 1) / chunks;
+  const int i0 = chunk * rpc, i1 = min(rows, i0 + rpc);
+  const double* a = F->x[mode][F->sel[mode]];
+  double* dst = part + ((size_t)mode * chunks + chunk) * r * r;
+  for (int e = threadIdx.x; e < r * r; e += blockDim.x) {
+    const int p = e / r, q = e % r;
+    double s0 = 0.0, s1 = 0.0;
+    int i = i0;
+    for (; i + 1 < i1; i += 2) {
+      s0 += a[(long long)i * r + p] * a[(long long)i * r + q];
+      s1 += a[(long long)(i + 1) * r + p] * a[(long long)(i + 1) * r + q];
+    }
+    if (i < i1) s0 += a[(long long)i * r + p] * a[(long long)i * r + q];
+    dst[e] = s0 + s1;
+  }
+}
+
+__global__ void __launch_bounds__(kGramThreads) gram_finish_kernel(DevFactors* F, const double* __restrict__ part,
+                                                                   int chunks) {
+  const int mode = blockIdx.x, r = F->rank;
+  double* g = F->gram[mode][F->sel[mode]];
+  for (int e = threadIdx.x; e < r * r; e += blockDim.x) {
+    double t = 0.0;
+    for (int c = 0; c < chunks; ++c) t += part[((size_t)mode * chunks + c) * r * r + e];
+    g[e] = t;
+  }
+}
+
+// FP32 mirrors of both buffers of every mode (grid-stride, blockIdx.y = mode)
+__global__ void mirror_kernel(DevFactors* F) {
+  const int mode = blockIdx.y;
+  const long long n = (long long)F->rows[mode] * F->rank;
   for (int bb = 0; bb < 2; ++bb) {
     float* m = F->x32[mode][bb];
     const double* x = F->x[mode][bb];
     if (m && x)
-      for (long long e = threadIdx.x; e < (long long)rows * r; e += blockDim.x) m[e] = float(x[e]);
+      for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x)
+        m[e] = float(x[e]);
   }
 }
 
-// cheap_objective at `pivot` (kernels.cpp:298-303 with the pivot of :305-311).
+// cheap_objective at `pivot` (kernels.cpp:298-303 with the pivot of :305-311);
+// every Gram (the pivot's included) is current: launch_init_factors ran on
+// the same factors
 __global__ void __launch_bounds__(kSetupThreads) objective_kernel(const DevFactors* __restrict__ F, int order,
                                                                   int r, int pivot, int rows,
                                                                   const double* __restrict__ C,
                                                                   const double* __restrict__ nsq,
                                                                   double* __restrict__ out) {
-  extern __shared__ double sm[];  // ga[r*r], red[blockDim]
-  double* ga = sm;
-  double* red = sm + r * r;
+  __shared__ double red[kSetupThreads];
   const double* a = F->x[pivot][F->sel[pivot]];
-  gram_rows(a, rows, r, ga, red);
   double cross = 0.0;
   for (long long e = threadIdx.x; e < (long long)rows * r; e += blockDim.x) cross += a[e] * C[e];
   cross = block_sum(cross, red);
@@ -238,7 +235,7 @@ __global__ void __launch_bounds__(kSetupThreads) objective_kernel(const DevFacto
     double g = 1.0;
     for (int j = 0; j < order; ++j)
       if (j != pivot) g *= gp[j][e];
-    quad += ga[e] * g;
+    quad += gp[pivot][e] * g;
   }
   quad = block_sum(quad, red);
   if (threadIdx.x == 0) *out = 0.5 * (*nsq) - cross + 0.5 * quad;
@@ -299,17 +296,31 @@ void launch_norm_sq(const void* t, int dtype, long long n, double* scratch, int 
   NTF_CUDA(cudaGetLastError());
 }
 
-void launch_init_factors(DevFactors* dF, const DevFactors& hF, cudaStream_t s) {
-  init_factors_kernel<<<hF.order, kSetupThreads, 0, s>>>(dF);
+size_t init_factors_scratch(const DevFactors& hF) {
+  int rows = 1;
+  for (int i = 0; i < hF.order; ++i) rows = std::max(rows, hF.rows[i]);
+  const int chunks = std::max(1, std::min(64, (rows + kGramRows - 1) / kGramRows));
+  return size_t(hF.order) * chunks * hF.rank * hF.rank;
+}
+
+void launch_init_factors(DevFactors* dF, const DevFactors& hF, double* scratch, size_t scratch_len, cudaStream_t s) {
+  int rows = 1;
+  for (int i = 0; i < hF.order; ++i) rows = std::max(rows, hF.rows[i]);
+  int chunks = std::max(1, std::min(64, (rows + kGramRows - 1) / kGramRows));
+  const size_t per = size_t(hF.order) * hF.rank * hF.rank;
+  chunks = int(std::max<size_t>(1, std::min<size_t>(size_t(chunks), scratch_len / per)));
+  if (scratch_len < per) throw LogicError("init_factors scratch too small");
+  gram_partial_kernel<<<dim3(unsigned(hF.order), unsigned(chunks)), kGramThreads, 0, s>>>(dF, scratch, chunks);
+  gram_finish_kernel<<<unsigned(hF.order), kGramThreads, 0, s>>>(dF, scratch, chunks);
+  bool mirrors = false;
+  for (int i = 0; i < hF.order; ++i) mirrors = mirrors || hF.x32[i][0] || hF.x32[i][1];
+  if (mirrors) mirror_kernel<<<dim3(64u, unsigned(hF.order)), 256, 0, s>>>(dF);
   NTF_CUDA(cudaGetLastError());
 }
 
 void launch_objective(const DevFactors* dF, int order, int rank, int pivot, int rows, const double* C,
                       const double* nsq_dev, double* out, cudaStream_t s) {
-  const size_t smem = sizeof(double) * (size_t(rank) * rank + kSetupThreads);
-  if (smem > 48 * 1024)
-    NTF_CUDA(cudaFuncSetAttribute(objective_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-  objective_kernel<<<1, kSetupThreads, smem, s>>>(dF, order, rank, pivot, rows, C, nsq_dev, out);
+  objective_kernel<<<1, kSetupThreads, 0, s>>>(dF, order, rank, pivot, rows, C, nsq_dev, out);
   NTF_CUDA(cudaGetLastError());
 }
 

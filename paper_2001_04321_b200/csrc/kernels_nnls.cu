@@ -982,9 +982,11 @@ __global__ void __launch_bounds__(kStreamTPB, 1) nnls_stream_kernel(NnlsLaunch a
 #pragma unroll
       for (int w = 0; w < WN2; ++w) wr[j][w] = wins[j * WN2 + w];
     };
+    // coefficient rows are loaded PF steps ahead (a ring of PF + 1 rows in registers)
+    constexpr int PF = 2;
     load_row(RP - 1);
     load_row(0);
-    load_row(1);
+    if constexpr (PF == 2) load_row(1);
     auto wcoef = [&](int j, int d) -> double {  // h_{j,j+d} from the registers
       const double2 x = wr[j][(d - 1) / 2];
       return ((d - 1) & 1) ? x.y : x.x;
@@ -1046,7 +1048,7 @@ __global__ void __launch_bounds__(kStreamTPB, 1) nnls_stream_kernel(NnlsLaunch a
         } else {
           if (k == j % Q) P[j / Q] = rv[j / Q];
         }
-        load_row((j + 2) % RP);
+        load_row((j + PF) % RP);
         if (j == RP / 2) c = ld_volatile_u64(ctl);  // decisions so far, checked after the pass
       }
       pass_cyc += pclock() - tp0;

@@ -134,7 +134,8 @@ void launch_reduce_partials(const double* partial, int segs, long long n, double
 void launch_norm_sq(const void* t, int dtype, long long n, double* scratch, int scratch_len, double* out,
                     cudaStream_t s);
 // gram[i][b] = x[i][b]^T x[i][b] for every mode (b = sel) and FP32 mirrors.
-void launch_init_factors(DevFactors* dF, const DevFactors& hF, cudaStream_t s);
+void launch_init_factors(DevFactors* dF, const DevFactors& hF, double* scratch, size_t scratch_len, cudaStream_t s);
+size_t init_factors_scratch(const DevFactors& hF);  // doubles of scratch launch_init_factors wants
 // cheap objective at pivot: 0.5 nsq - <A,C> + 0.5 <A^T A, G>, G = hadamard of
 // the X-role Grams except `pivot` (kernels.cpp:298-311). Writes *out.
 void launch_objective(const DevFactors* dF, int order, int rank, int pivot, int rows, const double* C,

@@ -504,7 +504,11 @@ Session::Session(ntf_ctx* ctx, const ntf_tensor* t, int algo, const double* init
   // start the run clock (her.cpp:58 / ao.cpp:28).
   DevFactors* dF = dF_.as<DevFactors>();
   RunState* dst = state_.as<RunState>();
-  launch_init_factors(dF, hF_, stream_);
+  {
+    DevBuf gs(init_factors_scratch(hF_) * sizeof(double));
+    launch_init_factors(dF, hF_, gs.as<double>(), gs.bytes / sizeof(double), stream_);
+    NTF_CUDA(cudaStreamSynchronize(stream_));  // (gs is released below)
+  }
   eng_->run(order_ - 1, dF, C_.as<double>(), stream_);
   launch_objective(dF, order_, rank, order_ - 1, rows_[order_ - 1], C_.as<double>(), &dst->nsq, &dst->f0,
                    stream_);

@@ -159,7 +159,7 @@ struct CallCache {
   int rank = 0;
   unsigned flags = 0;
   std::unique_ptr<MttkrpEngine> eng;
-  DevBuf fac, fac32, grams, dF, C;
+  DevBuf fac, fac32, grams, dF, C, gscratch;
   DevFactors h{};
 };
 

@@ -163,9 +163,10 @@ def _instance(P, shape, rank, sigma, seed, ill=False):
 @pytest.mark.parametrize("shape,rank,sigma,seed", [([50, 50, 50], 10, 0.01, 101), ([30, 30, 30], 5, 0.0, 4000),
                                                    ([8, 7, 6], 3, 0.05, 7), ([20, 20, 20, 20], 4, 0.01, 103),
                                                    ([12, 9], 2, 0.01, 402), ([15, 12, 10], 4, 0.001, 97)])
-@pytest.mark.parametrize("flags", [0, 8], ids=["tree", "direct"])
+@pytest.mark.parametrize("flags", [0, 8, 16], ids=["tree", "direct", "tree-no-overlap"])
 def test_her_trace_parity(P, oracle, shape, rank, sigma, seed, flags):
-    """Default flags = the dimension tree; RUN_DIRECT = N full passes."""
+    """Default flags = the dimension tree with the overlapped 3-way pass;
+    RUN_DIRECT = N full passes; RUN_NO_OVERLAP = the tree without it."""
     t, truth, init = _instance(P, shape, rank, sigma, seed, ill=(seed == 97))
     cfg = P.AoConfig(max_outer_iters=50, flags=flags)
     model, trace = P.her_run(t, init, cfg, P.HerParams())
@@ -179,7 +180,8 @@ def test_her_trace_parity(P, oracle, shape, rank, sigma, seed, flags):
         assert rel_fro(a, b) < 1e-6
     e_gpu = P.factor_error(model, truth)
     e_ora = oracle.factor_error(fo, truth.factors)
-    assert abs(e_gpu - e_ora) <= 1e-6 * e_ora + 1e-12, (e_gpu, e_ora)
+    # e is a normalised error (<= ~2): the factors agree to 1e-6, so e to 1e-6 absolute
+    assert abs(e_gpu - e_ora) <= 1e-6, (e_gpu, e_ora)
 
 
 @pytest.mark.parametrize("shape,rank,sigma,seed", [([50, 50, 50], 10, 0.01, 101), ([6, 5, 4], 3, 0.1, 29),
