@@ -746,13 +746,16 @@ bool sk_choose(const ModeView& v, int dtype, int sms, SkPlan* out) {
     align = 1;
   }
   if (const char* e = std::getenv("NTF_SK_NMF")) nmf = std::atoi(e);
-  if (f32) {  // four warps of (32 / nnf) x 8 rows: 256 (r <= 32) or 128 (r <= 64) row tiles
-    mw = 4;
+  if (f32) {  // warps of (32 / nnf) x 8 rows: 4 x 64 (r <= 32) or 8 x 32 (r <= 64) = 256-row tiles
+    // (measured r02z: r = 64 gains from 8 warps -- C5 pass 24.0 -> 19.4 ms,
+    // 0.70 of the FFMA peak; r = 32 has no room for 8 x 64-row warps' stages)
+    mw = nnf == 8 ? 8 : 4;
+    if (const char* e = std::getenv("NTF_SK_MW")) mw = std::atoi(e) == 8 ? 8 : 4;
     nmf = 1;
     align = 0;
   }
   if (const char* e = std::getenv("NTF_SK_ALIGN")) align = std::atoi(e);
-  const int m_cta = f32 ? 4 * (32 / nnf) * 8 : rows_per_frag_set * nmf;
+  const int m_cta = f32 ? mw * (32 / nnf) * 8 : rows_per_frag_set * nmf;
   if (f32 && (v.I + m_cta - 1) / m_cta >= 4LL * sms && !std::getenv("NTF_SK_ALIGN")) align = 1;
   SkPlan pl;
   SkParams& p = pl.p;

@@ -323,6 +323,11 @@ std::string MttkrpEngine::describe(int mode) const {
 
 int MttkrpEngine::kernels_per_call(int mode) const {
   if (tucker_) return 2 + core_eng_->kernels_per_call(mode);
+  if (overlap_) {  // Y_L pass + contraction | contraction + the overlapped P_0 pass | contraction
+    if (mode == 0) return 1 + std::min(2, fast_mttkrp_kernels(ttm_view_, t_->dtype));
+    if (mode == 1) return 1 + std::min(2, fast_mttkrp_kernels(p0_view_, t_->dtype));
+    return 1;
+  }
   // the fast kernel reduces its split-K slabs itself (the engine passes an
   // arrival counter) unless NTF_FAST_SEPARATE_REDUCE asks for the old kernel
   const int fast_kernels = std::getenv("NTF_FAST_SEPARATE_REDUCE") ? 2 : 1;
