@@ -390,7 +390,8 @@ def run_ours(args):
                          "bytes_per_launch": bytes_per, "avg_launch_ms": avg_ms,
                          "per_mode_ms": per_mode_ms,
                          "fma_tflops": flops_per / (avg_ms / 1e3) / 1e12,
-                         "fma_peak_tflops": fp32_peak if dt == "f32" else fp64_peak},
+                         "fma_peak_tflops": fp32_peak if dt == "f32" else fp64_peak,
+                         "fma_frac": flops_per / (avg_ms / 1e3) / 1e12 / (fp32_peak if dt == "f32" else fp64_peak)},
             "e2e": {"value": args.steps / e2e_s, "unit": UNIT, "samples_s": e2e_samples, "host_memory": pinned,
                     "h2d_bytes_per_step": (t_local.nbytes + init.flat().nbytes) / args.steps,
                     "d2h_bytes_per_step": (init.flat().nbytes + 64 * args.steps) / args.steps},
