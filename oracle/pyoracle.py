@@ -14,6 +14,7 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB = None
+_LIB_FILE = "liboracle.so"  # oracle/pyref.py re-instantiates this module over oracle/_ref/libntf_ref.so
 
 _dptr = C.POINTER(C.c_double)
 _iptr = C.POINTER(C.c_int)
@@ -33,13 +34,16 @@ OBSERVER = C.CFUNCTYPE(None, C.c_void_p, C.c_int, C.c_double, C.c_int, C.c_doubl
 
 
 def build():
-    subprocess.run(["make", "-s", "-C", _HERE], check=True)
+    if _LIB_FILE == "liboracle.so":
+        subprocess.run(["make", "-s", "-C", _HERE], check=True)
+    else:  # the reference build (needs /root/reference; the GPU box uses the prebuilt file)
+        subprocess.run(["make", "-s", "-C", os.path.join(_HERE, "ref_build")], check=True)
 
 
 def lib():
     global _LIB
     if _LIB is None:
-        path = os.path.join(_HERE, "liboracle.so")
+        path = os.path.join(_HERE, _LIB_FILE)
         if not os.path.exists(path):
             build()
         L = C.CDLL(path)

@@ -80,11 +80,12 @@ __device__ __forceinline__ float2 ffma2(float a, float2 b, float2 c) {
 // the FP32 sums are added into FP64 (each lane its own entries: no race),
 // so no FP32 sum runs over more than flush_units * 32 terms (the FP32 bar of
 // BASELINE configs 4/5, mttkrp_fast_impl.cuh).
-template <int CG, int LAYOUT>
+template <int CG, int A, int LAYOUT>
 __device__ __forceinline__ void consume_f32(const SkParams& p, const unsigned char* t_base, const unsigned char* w_base,
                                             const unsigned char* aq_base, uint64_t* full, uint64_t* empty, long long w0,
                                             long long w1, long long U, const int* tile_ctas, int b, int cw, int lane) {
-  constexpr int RG = 32 / CG, A = 8, RW = RG * A, KB = 32;
+  static_assert(A == 4 || A == 8, "rows per lane");
+  constexpr int RG = 32 / CG, RW = RG * A, KB = 32;
   const int r = p.v.rank;
   const int rg = lane % RG, cg = lane / RG;
   auto lrow = [&](int i) {
@@ -176,13 +177,19 @@ __device__ __forceinline__ void consume_f32(const SkParams& p, const unsigned ch
     } else {
 #pragma unroll 4
       for (int k = 0; k < KB; ++k) {
-        const float4 ta = *reinterpret_cast<const float4*>(ts + roff[0] + k * tpitch);
-        const float4 tb = *reinterpret_cast<const float4*>(ts + roff[4] + k * tpitch);
+        float tv[A];
+#pragma unroll
+        for (int g = 0; g < A / 4; ++g) {
+          const float4 tq = *reinterpret_cast<const float4*>(ts + roff[4 * g] + k * tpitch);
+          tv[4 * g] = tq.x;
+          tv[4 * g + 1] = tq.y;
+          tv[4 * g + 2] = tq.z;
+          tv[4 * g + 3] = tq.w;
+        }
         const float4 a = *reinterpret_cast<const float4*>(wsb + k * bpitch + wcol);
         const float4 c = *reinterpret_cast<const float4*>(wsb + k * bpitch + wcol + 16);
         const float2 wv[4] = {make_float2(a.x, a.y), make_float2(a.z, a.w), make_float2(c.x, c.y),
                               make_float2(c.z, c.w)};
-        const float tv[A] = {ta.x, ta.y, ta.z, ta.w, tb.x, tb.y, tb.z, tb.w};
 #pragma unroll
         for (int i = 0; i < A; ++i)
 #pragma unroll
@@ -206,13 +213,16 @@ __device__ __forceinline__ void consume_f32(const SkParams& p, const unsigned ch
 
 // T = double: DMMA consumers, NMF 8-row fragments x NNF 8-column fragments
 // per warp. T = float (FP32 tensors, FP32 factor mirrors): FFMA2 register
-// tiles of 8 rows x 8 columns per lane, NNF = column groups of 8 (RG = 32 /
-// NNF row groups), FP32 sums flushed into FP64 every p.flush_units units.
+// tiles of A rows x 8 columns per lane (A = 8, or 4 when NMF = 4: eight
+// 32-row warps instead of four 64-row ones for r <= 32), NNF = column groups
+// of 8 (RG = 32 / NNF row groups), FP32 sums flushed into FP64 every
+// p.flush_units units.
 template <typename T, int NMF, int NNF, int LAYOUT>
 __global__ void __launch_bounds__(32 * (kMaxNP + kMaxMW), 1) mttkrp_sk_kernel(const __grid_constant__ CUtensorMap tmap,
                                                                             SkParams p) {
   constexpr int KBT = 128 / int(sizeof(T));  // reduction indices per unit
-  constexpr int RW = sizeof(T) == 8 ? 8 * NMF : (32 / NNF) * 8;  // rows per consumer warp
+  constexpr int FA = NMF == 4 ? 4 : 8;                             // FP32: rows per lane
+  constexpr int RW = sizeof(T) == 8 ? 8 * NMF : (32 / NNF) * FA;  // rows per consumer warp
   extern __shared__ __align__(1024) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const ModeView& v = p.v;
@@ -426,7 +436,7 @@ __global__ void __launch_bounds__(32 * (kMaxNP + kMaxMW), 1) mttkrp_sk_kernel(co
   } else if (warp < NP + MW) {
     // ------------------------------------------------------------ consumers
     if constexpr (sizeof(T) == 4) {
-      consume_f32<NNF, LAYOUT>(p, t_base, reinterpret_cast<const unsigned char*>(w_base),
+      consume_f32<NNF, FA, LAYOUT>(p, t_base, reinterpret_cast<const unsigned char*>(w_base),
                                reinterpret_cast<const unsigned char*>(aq_base), full, empty, w0, w1, U,
                                tile_ctas, b, warp - NP, lane);
     } else {
@@ -635,8 +645,11 @@ SkLaunch pick_layout(int layout) {
   return layout == fast::kRow ? launch_sk<double, NMF, NNF, fast::kRow> : launch_sk<double, NMF, NNF, fast::kCol>;
 }
 
-// FP32: NNF = column groups of 8 (4: r <= 32, 8: r <= 64)
-SkLaunch pick_f32(int cg, int layout) {
+// FP32: NNF = column groups of 8 (4: r <= 32, 8: r <= 64); rows per lane 8 (NMF = 1) or 4 (NMF = 4)
+SkLaunch pick_f32(int cg, int layout, int arows = 8) {
+  if (cg == 4 && arows == 4)
+    return layout == fast::kRow ? launch_sk<float, 4, 4, fast::kRow> : launch_sk<float, 4, 4, fast::kCol>;
+  if (arows != 8) return nullptr;
   switch (cg) {
     case 4: return layout == fast::kRow ? launch_sk<float, 1, 4, fast::kRow> : launch_sk<float, 1, 4, fast::kCol>;
     case 8: return layout == fast::kRow ? launch_sk<float, 1, 8, fast::kRow> : launch_sk<float, 1, 8, fast::kCol>;
@@ -749,13 +762,18 @@ bool sk_choose(const ModeView& v, int dtype, int sms, SkPlan* out) {
   if (f32) {  // warps of (32 / nnf) x 8 rows: 4 x 64 (r <= 32) or 8 x 32 (r <= 64) = 256-row tiles
     // (measured r02z: r = 64 gains from 8 warps -- C5 pass 24.0 -> 19.4 ms,
     // 0.70 of the FFMA peak; r = 32 has no room for 8 x 64-row warps' stages)
-    mw = nnf == 8 ? 8 : 4;
+    // r <= 32: eight warps of 32 rows (4 rows x 8 columns per lane) -- two
+    // warps per SM sub-partition hide each other's operand loads and barrier
+    // waits, the same 256-row stages as four 64-row warps (NTF_SK_F32A=8)
+    mw = 8;
     if (const char* e = std::getenv("NTF_SK_MW")) mw = std::atoi(e) == 8 ? 8 : 4;
-    nmf = 1;
+    nmf = nnf == 4 && mw == 8 ? 4 : 1;
+    if (const char* e = std::getenv("NTF_SK_F32A")) nmf = (std::atoi(e) == 4 && nnf == 4) ? 4 : 1;
+    if (nnf == 4 && nmf == 1 && !std::getenv("NTF_SK_MW")) mw = 4;  // 64-row warps: four (stage room)
     align = 0;
   }
   if (const char* e = std::getenv("NTF_SK_ALIGN")) align = std::atoi(e);
-  const int m_cta = f32 ? mw * (32 / nnf) * 8 : rows_per_frag_set * nmf;
+  const int m_cta = f32 ? mw * (32 / nnf) * (nmf == 4 ? 4 : 8) : rows_per_frag_set * nmf;
   if (f32 && (v.I + m_cta - 1) / m_cta >= 4LL * sms && !std::getenv("NTF_SK_ALIGN")) align = 1;
   SkPlan pl;
   SkParams& p = pl.p;
@@ -766,6 +784,10 @@ bool sk_choose(const ModeView& v, int dtype, int sms, SkPlan* out) {
   if (const char* e = std::getenv("NTF_SK_NP")) p.NP = std::max(1, std::min(sk::kMaxNP, std::atoi(e)));
   p.m_cta = m_cta;
   p.n_mbox = (m_cta + 255) / 256;
+  // FP64 COL boxes need 4 spare elements for the conflict-free row pitch
+  // (m_box + 4 <= 256, the TMA box limit): a 256-row tile takes two boxes
+  // (r02ab capture at C3: 19.2 M of 28.6 M shared wavefronts were conflicts)
+  if (!f32 && layout == fast::kCol && m_cta / p.n_mbox + 4 > 256 && !std::getenv("NTF_SK_ONEBOX")) p.n_mbox *= 2;
   p.m_box = m_cta / p.n_mbox;
   if (p.m_box * p.n_mbox != m_cta || p.m_box % 8) return false;
   p.wld = 8 * nnf + 4;  // 32 B off the 64-byte bank period (4 k rows per half-warp)
@@ -826,7 +848,7 @@ bool sk_choose(const ModeView& v, int dtype, int sms, SkPlan* out) {
   pl.nmf = nmf;
   pl.nnf = nnf;
   pl.f32 = f32;
-  if (!(f32 ? sk::pick_f32(nnf, layout) : sk::pick(nmf, nnf, layout))) return false;
+  if (!(f32 ? sk::pick_f32(nnf, layout, nmf == 4 ? 4 : 8) : sk::pick(nmf, nnf, layout))) return false;
   // contributors per tile and the split tiles
   pl.tile_ctas.assign(size_t(2 * p.n_tiles), 0);
   for (int t = 0; t < p.n_tiles; ++t) {
@@ -913,8 +935,8 @@ void sk_mttkrp(const void* t, const ModeView& v, const SkPlan& pl, const DevFact
   p.rowL_wrap = modes.rowL_wrap;
   p.pdl = pdl && !p.n_split ? 1 : 0;  // (a cooperative split-tile launch is never a dependent)
   if (p.n_split && !counter) throw LogicError("stream-K MTTKRP needs an arrival counter");
-  (pl.f32 ? sk::pick_f32(pl.nnf, pl.layout) : sk::pick(pl.nmf, pl.nnf, pl.layout))(map, p, pl.grid, pl.threads, pl.smem,
-                                                                                   s);
+  (pl.f32 ? sk::pick_f32(pl.nnf, pl.layout, pl.nmf == 4 ? 4 : 8) : sk::pick(pl.nmf, pl.nnf, pl.layout))(
+      map, p, pl.grid, pl.threads, pl.smem, s);
 }
 
 std::string sk_describe(const SkPlan& pl) {

@@ -28,6 +28,15 @@ random_init(shape, r, stream_seed(S, 1))):
 
 Run: OMP_NUM_THREADS=<cores> python tests/golden/make_config_golden.py [c2 c3 c4]
 (about 1-10 minutes per config on 8 cores; commit the .npz files).
+
+`--ref` runs THE REFERENCE ITSELF instead of the oracle: oracle/_ref/
+libntf_ref.so, the unmodified /root/reference/proj sources compiled by
+oracle/ref_build/Makefile (Eigen stand-in; the reference's own unit suites
+pass over that build), through oracle/pyref.py, and writes refrun_*.npz with
+the same layout. Those are the reference-produced golden vectors the GPU
+parity tests and tests/test_ref_build.py compare against. (The collinear c4
+instance comes from this repo's generator -- the rule is SURVEY 8(d)'s, not a
+reference option -- and is handed to the reference as data.)
 """
 import os
 import sys
@@ -40,6 +49,12 @@ ROOT = os.path.dirname(os.path.dirname(HERE))
 sys.path.insert(0, os.path.join(ROOT, "oracle"))
 
 import pyoracle as ora  # noqa: E402
+
+REF = "--ref" in sys.argv
+if REF:
+    import pyref as run_impl  # noqa: E402
+else:
+    run_impl = ora
 
 ITERS = 50
 CONFIGS = {
@@ -60,10 +75,10 @@ def make(name):
     flat = t.reshape(-1)
     out = {"shape": np.array(shape), "rank": np.array(rank), "sigma": np.array(sigma),
            "seed": np.array(seed), "dtype": np.array(dt), "collinear": np.array(collinear),
-           "iters": np.array(ITERS), "norm_sq": np.array(ora.norm_sq(t)),
+           "iters": np.array(ITERS), "norm_sq": np.array(run_impl.norm_sq(t)),
            "t_head": np.array(flat[:64], np.float64), "t_tail": np.array(flat[-64:], np.float64)}
     for algo in ("her", "ao"):
-        fac, f0, recs = ora.run(algo, t, init, max_outer_iters=ITERS)
+        fac, f0, recs = run_impl.run(algo, t, init, max_outer_iters=ITERS)
         out[f"{algo}_f0"] = np.array(f0)
         out[f"{algo}_f"] = np.array([r["f"] for r in recs])
         if algo == "her":
@@ -71,14 +86,14 @@ def make(name):
             out["her_beta"] = np.array([r["beta"] for r in recs])
         for i, a in enumerate(fac):
             out[f"{algo}_final{i}"] = a
-        out[f"{algo}_e"] = np.array(ora.factor_error(fac, truth))
+        out[f"{algo}_e"] = np.array(run_impl.factor_error(fac, truth))
         print(f"{name} {algo}: f0={f0:.6e} f50={recs[-1]['f']:.6e} e50={float(out[f'{algo}_e']):.6e}",
               flush=True)
-    path = os.path.join(HERE, f"config_{name}.npz")
+    path = os.path.join(HERE, f"{'refrun' if REF else 'config'}_{name}.npz")
     np.savez_compressed(path, **out)
     print(f"{path}: {os.path.getsize(path)} bytes, {time.time() - t0:.1f} s", flush=True)
 
 
 if __name__ == "__main__":
-    for name in (sys.argv[1:] or list(CONFIGS)):
+    for name in ([a for a in sys.argv[1:] if not a.startswith("--")] or list(CONFIGS)):
         make(name)

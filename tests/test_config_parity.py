@@ -51,8 +51,10 @@ def _exact_f0(name):
         return json.load(fh)[name]
 
 
-def _fixture(name):
-    path = os.path.join(HERE, "golden", f"config_{name}.npz")
+def _fixture(name, kind="config"):
+    """kind "config": the oracle's run; "refrun": the same run by the
+    reference itself (oracle/_ref, make_config_golden.py --ref)."""
+    path = os.path.join(HERE, "golden", f"{kind}_{name}.npz")
     return dict(np.load(path, allow_pickle=False))
 
 
@@ -100,9 +102,14 @@ def test_config_fixtures_cover_the_north_star_configs():
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("algo", ["her", "ao"])
+@pytest.mark.parametrize("kind", ["config", "refrun"])
 @pytest.mark.parametrize("name", CONFIGS)
-def test_config_trace_parity(P, instances, name, algo):
+def test_config_trace_parity(P, instances, name, algo, kind):
+    """kind "config": against the oracle restatement's run; "refrun": against
+    the run of the reference itself (its own sources, oracle/ref_build)."""
     g, t, truth, init = instances(name)
+    if kind == "refrun":
+        g = _fixture(name, "refrun")
     flat = t.reshape(-1)
     assert np.array_equal(np.asarray(flat[:64], np.float64), g["t_head"])
     assert np.array_equal(np.asarray(flat[-64:], np.float64), g["t_tail"])
@@ -125,7 +132,7 @@ def test_config_trace_parity(P, instances, name, algo):
     e_gpu = P.factor_error(model, truth)
     e_ora = float(g[f"{algo}_e"])
     finals = [g[f"{algo}_final{i}"] for i in range(len(init.factors))]
-    report = {"config": name, "algo": algo, "f0_rel": abs(trace.f0 - f0o) / abs(f0o),
+    report = {"config": name, "algo": algo, "against": kind, "f0_rel": abs(trace.f0 - f0o) / abs(f0o),
               "f_rel": (np.abs(fg - fo) / np.abs(fo)).tolist(), "f_abs_over_nsq": (np.abs(fg - fo) / nsq).tolist(),
               "e_gpu": e_gpu, "e_oracle": e_ora, "final_rel_fro": [rel_fro(a, b) for a, b in zip(model, finals)]}
     if algo == "her":
