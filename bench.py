@@ -15,9 +15,12 @@ flush is needed). ``e2e`` is the same metric through the public C-ABI driver
 ntf_her_run with host buffers: upload of the tensor and init, K iterations,
 download of factors and trace inside the timed region.
 
-``--impl reference`` times the reference algorithm's CPU implementation (the
-oracle restatement in oracle/, built with OpenMP over all host cores, because
-the reference itself cannot be compiled without Eigen3) on the same config.
+``--impl reference`` times the reference algorithm's CPU implementation on the
+same config: the oracle restatement in oracle/ (OpenMP over all host cores),
+which is pinned to the reference's own sources built in oracle/_ref
+(tests/test_ref_build.py). That build links a minimal Eigen stand-in whose
+temporaries make it ~10x slower than the restatement at config scale, so
+timing it would understate the reference; kind stays "port".
 
 Multi-GPU (torchrun, one rank per GPU): the tensor is slab-sharded along
 mode 1; per-GPU work shrinks with N (strong scaling of one instance).
@@ -231,8 +234,10 @@ def run_reference_arm(args):
         "config": workload_config(args.config, args.algo),
         "cpu_baseline": {"value": rate, "unit": UNIT, "cores": cores, "kind": "port", "cpu": cpu_model(),
                          "sample": f"{args.warmup}+{args.steps} outer iterations of the full instance; the "
-                                   "reference (needs Eigen3) cannot be built, so the oracle restatement of its "
-                                   "algorithm runs (OpenMP over output rows, materialised Khatri-Rao)"},
+                                   "oracle restatement of the reference algorithm runs (OpenMP over output "
+                                   "rows, materialised Khatri-Rao); it is pinned to the reference's own sources "
+                                   "built against an Eigen stand-in (oracle/_ref), which is a checker, not a "
+                                   "fair timing target"},
         "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)

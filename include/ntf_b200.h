@@ -192,6 +192,21 @@ int ntf_slab_range(int64_t dim0, int rank, int world, int64_t* begin, int64_t* e
  * once in FP64 (DenseProvider ctor, provider.cpp:7; tensor.cpp:43-47). */
 int ntf_tensor_upload(ntf_ctx* ctx, const void* host, int dtype, int order, const int64_t* shape,
                       ntf_tensor** out);
+/* The same without blocking the host: returns once the copy and the ||T||^2
+ * reduction are ENQUEUED on the context's stream, so the caller's next calls
+ * (ntf_her_run / ntf_ao_run / ntf_session_create: engine tables, buffers,
+ * first launches, CUDA-graph capture) overlap the transfer; every consumer is
+ * ordered after it on the device. Contract: `host` must stay valid and
+ * unmodified until ntf_tensor_wait(t) returns or a later call on this handle
+ * has returned tensor-derived data to the host (ntf_tensor_norm_sq, ntf_mttkrp*,
+ * a driver run). With pageable memory the CUDA runtime stages the copy
+ * synchronously and nothing is gained; use pinned memory (cudaHostAlloc /
+ * cudaHostRegister). DenseProvider takes its tensor by reference too
+ * (provider.hpp:24-33: "does not own it"). */
+int ntf_tensor_upload_async(ntf_ctx* ctx, const void* host, int dtype, int order, const int64_t* shape,
+                            ntf_tensor** out);
+/* Blocks until the upload of `t` (and its ||T||^2) has completed. */
+int ntf_tensor_wait(const ntf_tensor* t);
 /* Same, from a device buffer of this context's GPU (copied). Ordering: the
  * copy runs on the context's own stream, so the caller's producer work must
  * be complete -- this entry point synchronises the device before copying.

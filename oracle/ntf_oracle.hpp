@@ -8,17 +8,23 @@
 // product library (paper_2001_04321_b200/libntf_b200.so) never links, loads or
 // calls anything in oracle/.
 //
-// Parity pinning: the reference cannot be compiled here (Eigen3, doctest and
-// CLI11 are absent), and it ships no stored golden
-// data. This oracle is pinned against every known-answer test and property
-// test the reference's own suites hold for the path (std::mt19937_64 10000th
-// draw, rank-one MTTKRP identity, Hadamard-of-Grams == KR^T KR, cheap
-// objective == residual, HALS scalar formula, update_betas arithmetic, beta->0
-// reduction to AO, restart bookkeeping, determinism) — see tests/test_oracle.py
-// — and against an independent numpy restatement (tests/golden/make_golden.py).
-// Arithmetic that the reference delegates to Eigen (GEMV inside hals_pass,
-// Gram GEMM, Frobenius norms, redux sums) is restated in plain ascending
-// order, so agreement with the reference is "to rounding", not bitwise.
+// Parity pinning: the reference's CMake build needs Eigen3, doctest, CLI11 and
+// nlohmann-json (absent from the image), but its hot-path sources compile,
+// unmodified and from where they lie, against the small Eigen stand-in of
+// oracle/ref_build/ into oracle/_ref/libntf_ref.so, and the reference's own
+// unit suites pass over that build. This oracle is pinned to that build
+// function by function and trace by trace (tests/test_ref_build.py: datagen
+// bit for bit, MTTKRP, HALS / every inner solver, whole her_run / ao_run traces
+// with identical restart decisions and final factors), to the reference-
+// produced runs at the BASELINE configs (tests/golden/refrun_c*.npz), and to
+// every known-answer and property test the reference's own suites hold for
+// the path (std::mt19937_64 10000th draw, rank-one MTTKRP identity,
+// Hadamard-of-Grams == KR^T KR, cheap objective == residual, HALS scalar
+// formula, update_betas arithmetic, beta->0 reduction to AO, restart
+// bookkeeping, determinism; tests/test_oracle.py). Arithmetic the reference
+// delegates to Eigen (GEMV inside hals_pass, Gram GEMM, Frobenius norms,
+// redux sums) is restated in plain ascending order -- as the stand-in does --
+// so agreement with a real Eigen build is "to rounding", not bitwise.
 //
 // Storage conventions (shared with the product's C ABI):
 //   * tensors: row-major, last index fastest (tensor.hpp:11-13);

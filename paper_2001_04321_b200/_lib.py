@@ -89,6 +89,8 @@ SIGNATURES = {
     "ntf_ctx_destroy": (C.c_int, [C.c_void_p]),
     "ntf_slab_range": (C.c_int, [C.c_int64, C.c_int, C.c_int, i64ptr, i64ptr]),
     "ntf_tensor_upload": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, i64ptr, C.POINTER(C.c_void_p)]),
+    "ntf_tensor_upload_async": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, i64ptr, C.POINTER(C.c_void_p)]),
+    "ntf_tensor_wait": (C.c_int, [C.c_void_p]),
     "ntf_tensor_upload_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, i64ptr,
                                            C.POINTER(C.c_void_p)]),
     "ntf_tensor_upload_device_async": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, i64ptr, C.c_void_p,

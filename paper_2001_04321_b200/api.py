@@ -493,8 +493,12 @@ class GpuDenseProvider(ObjectiveProvider):
             shape = list(full_shape or t.shape)
             code = L.NTF_DTYPE_F32 if t.dtype == np.float32 else L.NTF_DTYPE_F64
             arr = (C.c_int64 * len(shape))(*shape)
-            _check(L.lib().ntf_tensor_upload(self.ctx.handle, t.ctypes.data_as(C.c_void_p), code, len(shape),
-                                             arr, C.byref(h)))
+            # enqueue-only upload: the copy from pinned host memory overlaps the
+            # caller's next calls (her_run's setup and graph capture); the array
+            # is kept alive until the provider is closed (ntf_b200.h contract)
+            self._source = t
+            _check(L.lib().ntf_tensor_upload_async(self.ctx.handle, t.ctypes.data_as(C.c_void_p), code, len(shape),
+                                                   arr, C.byref(h)))
         self.handle = h
         self._shape = [int(d) for d in shape]
         self.dtype = np.float32 if code == L.NTF_DTYPE_F32 else np.float64
@@ -564,10 +568,15 @@ class GpuDenseProvider(ObjectiveProvider):
         _check(L.lib().ntf_objective(self.ctx.handle, self.handle, _dp(flat), m.rank(), pivot, C.byref(out)))
         return out.value
 
+    def wait(self):
+        """Block until the tensor's upload (and its ||T||^2) has completed."""
+        _check(L.lib().ntf_tensor_wait(self.handle))
+
     def close(self):
         if getattr(self, "handle", None):
-            L.lib().ntf_tensor_destroy(self.handle)
+            L.lib().ntf_tensor_destroy(self.handle)  # synchronises the context's stream first
             self.handle = None
+        self._source = None
 
     def __del__(self):
         try:

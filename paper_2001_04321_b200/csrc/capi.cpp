@@ -110,9 +110,23 @@ void check_run_inputs(const ntf_tensor* t, const double* init, int rank, const n
 // all-reduced over the ranks).
 // rows = {begin, end} picks a caller-chosen mode-1 slab on a 1-GPU context
 // (ntf_tensor_upload_rows); {-1, -1} = this rank's slab_range.
+// The host value of ||T||^2: fetched on first use after an asynchronous upload.
+double host_nsq(const ntf_tensor* t) {
+  if (!t->nsq_valid) {
+    NTF_CUDA(cudaSetDevice(t->ctx->device));
+    NTF_CUDA(cudaMemcpyAsync(&t->nsq, t->nsq_dev.p, sizeof(double), cudaMemcpyDeviceToHost, t->ctx->stream));
+    NTF_CUDA(cudaStreamSynchronize(t->ctx->stream));
+    t->nsq_valid = true;
+  }
+  return t->nsq;
+}
+
+// async: return once the copy and the ||T||^2 reduction are enqueued on
+// ctx->stream (ntf_tensor_upload_async); `ready` marks their completion for
+// consumers on other streams (Session).
 template <typename Fill>
 ntf_tensor* make_tensor_with(ntf_ctx* ctx, int dtype, int order, const int64_t* shape, Fill&& fill,
-                             long long rows_b = -1, long long rows_e = -1) {
+                             long long rows_b = -1, long long rows_e = -1, bool async = false) {
   need(ctx, "ctx");
   need(shape, "shape");
   if (dtype != NTF_DTYPE_F64 && dtype != NTF_DTYPE_F32) throw InvalidArgument("unknown dtype");
@@ -149,8 +163,14 @@ ntf_tensor* make_tensor_with(ntf_ctx* ctx, int dtype, int order, const int64_t* 
     launch_norm_sq(t->data.p, dtype, t->n_local, ctx->scratch.as<double>(), int(ctx->scratch.bytes / 8),
                    t->nsq_dev.as<double>(), ctx->stream);
     ctx->comm.allreduce_sum(t->nsq_dev.as<double>(), 1, ctx->stream);
-    NTF_CUDA(cudaMemcpyAsync(&t->nsq, t->nsq_dev.p, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
-    NTF_CUDA(cudaStreamSynchronize(ctx->stream));
+    NTF_CUDA(cudaEventCreateWithFlags(&t->ready, cudaEventDisableTiming));
+    NTF_CUDA(cudaEventRecord(t->ready, ctx->stream));
+    if (async) {
+      t->nsq_valid = false;
+    } else {
+      NTF_CUDA(cudaMemcpyAsync(&t->nsq, t->nsq_dev.p, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+      NTF_CUDA(cudaStreamSynchronize(ctx->stream));
+    }
   } catch (...) {
     delete t;
     throw;
@@ -159,7 +179,7 @@ ntf_tensor* make_tensor_with(ntf_ctx* ctx, int dtype, int order, const int64_t* 
 }
 
 ntf_tensor* make_tensor(ntf_ctx* ctx, const void* src, bool src_on_device, int dtype, int order,
-                        const int64_t* shape, long long rows_b = -1, long long rows_e = -1) {
+                        const int64_t* shape, long long rows_b = -1, long long rows_e = -1, bool async = false) {
   need(src, "tensor data");
   return make_tensor_with(
       ctx, dtype, order, shape,
@@ -168,7 +188,7 @@ ntf_tensor* make_tensor(ntf_ctx* ctx, const void* src, bool src_on_device, int d
         NTF_CUDA(cudaMemcpyAsync(t->data.p, src, size_t(t->n_local) * es,
                                  src_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, ctx->stream));
       },
-      rows_b, rows_e);
+      rows_b, rows_e, async);
 }
 
 // The per-call provider workspace of tensor t for (rank, flags): engine,
@@ -477,6 +497,21 @@ int ntf_tensor_upload(ntf_ctx* ctx, const void* host, int dtype, int order, cons
   });
 }
 
+int ntf_tensor_upload_async(ntf_ctx* ctx, const void* host, int dtype, int order, const int64_t* shape,
+                            ntf_tensor** out) {
+  return guarded([&] {
+    need(out, "out");
+    *out = make_tensor(ctx, host, false, dtype, order, shape, -1, -1, true);
+  });
+}
+
+int ntf_tensor_wait(const ntf_tensor* t) {
+  return guarded([&] {
+    need(t, "tensor");
+    if (t->ready) NTF_CUDA(cudaEventSynchronize(t->ready));
+  });
+}
+
 int ntf_tensor_upload_ntft(ntf_ctx* ctx, const char* path, int dtype, ntf_tensor** out) {
   return guarded([&] {
     need(out, "out");
@@ -677,7 +712,7 @@ int ntf_tensor_norm_sq(const ntf_tensor* t, double* out) {
   return guarded([&] {
     need(t, "tensor");
     need(out, "out");
-    *out = t->nsq;
+    *out = host_nsq(t);
   });
 }
 

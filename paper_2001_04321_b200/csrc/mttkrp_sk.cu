@@ -142,6 +142,86 @@ __device__ __forceinline__ void consume_f32(const SkParams& p, const unsigned ch
     started = !seg_end;
     since = 0;
   };
+  if constexpr (A == 4) {
+    // Software-pipelined 4-k steps: the operands of step kq + 1 (4 T reads +
+    // 8 W reads of 16 bytes, 48 registers) are loaded before the 64 FFMA2 of
+    // step kq, across unit boundaries too (the next stage's first step is
+    // loaded right after this stage's last operands are in registers and the
+    // stage is released), so a warp's shared-memory latency hides behind its
+    // own FMAs as well as behind the sub-partition's second warp.
+    struct Ops {
+      float4 t[A];
+      float4 w[8];
+    };
+    auto stage_t = [&](int st) { return t_base + size_t(st) * p.t_stage_bytes; };
+    auto stage_w = [&](int st) {
+      return p.direct_b ? aq_base + size_t(st) * p.aq_stage_bytes : w_base + size_t(st) * p.w_stage_bytes;
+    };
+    auto load_ops = [&](const unsigned char* ts, const unsigned char* wsb, int kq, Ops& o) {
+#pragma unroll
+      for (int i = 0; i < A; ++i) {
+        if (LAYOUT == fast::kRow) {
+          const int key = (roff[i] >> 7) & 7;
+          o.t[i] = *reinterpret_cast<const float4*>(ts + roff[i] + (((kq ^ key) & 7) << 4));  // four k of row i
+        } else {
+          o.t[i] = *reinterpret_cast<const float4*>(ts + roff[0] + (4 * kq + i) * tpitch);  // four rows of k = 4 kq + i
+        }
+      }
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        o.w[2 * kk] = *reinterpret_cast<const float4*>(wsb + (4 * kq + kk) * bpitch + wcol);
+        o.w[2 * kk + 1] = *reinterpret_cast<const float4*>(wsb + (4 * kq + kk) * bpitch + wcol + 16);
+      }
+    };
+    auto comp = [](const float4& v, int c) { return c == 0 ? v.x : c == 1 ? v.y : c == 2 ? v.z : v.w; };
+    auto compute = [&](const Ops& o) {
+#pragma unroll
+      for (int i = 0; i < A; ++i)
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+          const float tv = LAYOUT == fast::kRow ? comp(o.t[i], kk) : comp(o.t[kk], i);
+          acc[i][0] = ffma2(tv, make_float2(o.w[2 * kk].x, o.w[2 * kk].y), acc[i][0]);
+          acc[i][1] = ffma2(tv, make_float2(o.w[2 * kk].z, o.w[2 * kk].w), acc[i][1]);
+          acc[i][2] = ffma2(tv, make_float2(o.w[2 * kk + 1].x, o.w[2 * kk + 1].y), acc[i][2]);
+          acc[i][3] = ffma2(tv, make_float2(o.w[2 * kk + 1].z, o.w[2 * kk + 1].w), acc[i][3]);
+        }
+    };
+    Ops oa, ob;
+    if (w0 < w1) {
+      mbar_wait(&full[s], phase);
+      load_ops(stage_t(s), stage_w(s), 0, oa);
+    }
+    for (long long w = w0; w < w1; ++w) {
+      const unsigned char* ts = stage_t(s);
+      const unsigned char* wsb = stage_w(s);
+#pragma unroll
+      for (int kq = 0; kq < KB / 4; kq += 2) {
+        load_ops(ts, wsb, kq + 1, ob);
+        compute(oa);
+        if (kq + 2 < KB / 4) {
+          load_ops(ts, wsb, kq + 2, oa);
+        } else {
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty[s]);  // every operand of this stage is in registers
+          if (++s == p.stages) {
+            s = 0;
+            phase ^= 1;
+          }
+          if (w + 1 < w1) {
+            mbar_wait(&full[s], phase);
+            load_ops(stage_t(s), stage_w(s), 0, oa);
+          }
+        }
+        compute(ob);
+      }
+      const bool seg_end = ++u_in == U || w + 1 == w1;
+      if (seg_end || (p.flush_units > 0 && ++since == p.flush_units)) flush(seg_end);
+      if (seg_end) {
+        u_in = 0;
+        ++tile;
+      }
+    }
+  } else {
   for (long long w = w0; w < w1; ++w) {
     mbar_wait(&full[s], phase);
     const unsigned char* ts = t_base + size_t(s) * p.t_stage_bytes;
@@ -209,6 +289,7 @@ __device__ __forceinline__ void consume_f32(const SkParams& p, const unsigned ch
       ++tile;
     }
   }
+  }  // A == 8
 }
 
 // T = double: DMMA consumers, NMF 8-row fragments x NNF 8-column fragments

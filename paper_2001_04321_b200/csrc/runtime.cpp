@@ -489,7 +489,7 @@ Session::Session(ntf_ctx* ctx, const ntf_tensor* t, int algo, const double* init
   RunState st{};
   st.beta = params ? params->beta0 : 0.0;
   st.beta_bar = 1.0;
-  st.nsq = t->nsq;
+  st.nsq = 0.0;  // copied from the tensor's device value below
   if (params) {
     st.beta0 = params->beta0;
     st.gamma = params->gamma;
@@ -506,20 +506,26 @@ Session::Session(ntf_ctx* ctx, const ntf_tensor* t, int algo, const double* init
   NTF_CUDA(cudaMemcpyAsync(state_.p, &st, sizeof st, cudaMemcpyHostToDevice, stream_));
 
   // GramCache::create + pivot objective f0 (driver_common.hpp:50-56), then
-  // start the run clock (her.cpp:58 / ao.cpp:28).
+  // start the run clock (her.cpp:58 / ao.cpp:28). No host synchronisation:
+  // everything above (small uploads from pageable memory, run on an idle
+  // stream) and the Gram setup precede the wait for the tensor, so after an
+  // asynchronous upload (ntf_tensor_upload_async) this constructor, the first
+  // iteration's launches and the graph capture all overlap the host-to-device
+  // copy of the tensor; f0's MTTKRP starts when the copy and the ||T||^2
+  // reduction have finished (t->ready).
   DevFactors* dF = dF_.as<DevFactors>();
   RunState* dst = state_.as<RunState>();
-  {
-    DevBuf gs(init_factors_scratch(hF_) * sizeof(double));
-    launch_init_factors(dF, hF_, gs.as<double>(), gs.bytes / sizeof(double), stream_);
-    NTF_CUDA(cudaStreamSynchronize(stream_));  // (gs is released below)
-  }
+  init_scratch_ = DevBuf(init_factors_scratch(hF_) * sizeof(double));
+  launch_init_factors(dF, hF_, init_scratch_.as<double>(), init_scratch_.bytes / sizeof(double), stream_);
+  const ntf_tensor* deps[2] = {t, t->core.get()};
+  for (const ntf_tensor* dep : deps)
+    if (dep && dep->ready) NTF_CUDA(cudaStreamWaitEvent(stream_, dep->ready, 0));
+  NTF_CUDA(cudaMemcpyAsync(&dst->nsq, t->nsq_dev.p, sizeof(double), cudaMemcpyDeviceToDevice, stream_));
   eng_->run(order_ - 1, dF, C_.as<double>(), stream_);
   launch_objective(dF, order_, rank, order_ - 1, rows_[order_ - 1], C_.as<double>(), &dst->nsq, &dst->f0,
                    stream_);
   NTF_CUDA(cudaMemcpyAsync(&dst->f_prev, &dst->f0, sizeof(double), cudaMemcpyDeviceToDevice, stream_));
   launch_stamp_start(dst, stream_);
-  NTF_CUDA(cudaStreamSynchronize(stream_));
   if (timing) {
     const auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
     fprintf(stderr, "[ntf timing] session: stream %.2f ms, engine %.2f ms, buffers+init+f0 %.2f ms\n",
@@ -761,7 +767,9 @@ void Session::kernel_times(double* ms_per_mode, int* launches, int* total_kernel
 
 }  // namespace ntfb
 
-ntf_tensor::~ntf_tensor() = default;
+ntf_tensor::~ntf_tensor() {
+  if (ready) cudaEventDestroy(ready);
+}
 
 ntf_ctx::~ntf_ctx() {
   if (stream) cudaStreamDestroy(stream);

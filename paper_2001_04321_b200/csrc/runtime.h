@@ -207,6 +207,7 @@ class Session {
   DevFactors hF_{};
   DevBuf dF_, fac_, fac32_, grams_, C_, state_, trace_, scratch_, counter_;
   DevBuf solve_buf_, solve_work_;  // another inner solver: its result rows and per-row state
+  DevBuf init_scratch_;            // partial Grams of the constructor's setup kernels (kept: no host sync there)
   int trace_cap_ = 0;
   cudaGraph_t graph_ = nullptr;
   cudaGraphExec_t exec_ = nullptr;
@@ -242,7 +243,9 @@ struct ntf_tensor {
   long long n_local = 0;
   ntfb::DevBuf data;
   ntfb::DevBuf nsq_dev;  // ||T||^2 (global, FP64) on the device
-  double nsq = 0.0;
+  mutable double nsq = 0.0;       // host copy, valid once nsq_valid (ntfb::host_nsq fetches it lazily)
+  mutable bool nsq_valid = true;  // false after an asynchronous upload until the first host read
+  cudaEvent_t ready = nullptr;    // recorded on ctx->stream after the upload and the ||T||^2 reduction
   bool rows_only = false;  // a caller-chosen row slab on a 1-GPU context (ntf_tensor_upload_rows)
   mutable std::unique_ptr<ntfb::CallCache> cache;
   // TuckerProvider (kind == 1): the core as a dense device tensor, the bases

@@ -19,7 +19,7 @@ import pytest
 from parity import compare_traces, rel_fro
 
 HERE = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
-FIXTURES = sorted(p for p in glob.glob(os.path.join(HERE, "*.npz")) if not os.path.basename(p).startswith("config_"))
+FIXTURES = sorted(p for p in glob.glob(os.path.join(HERE, "*.npz")) if not os.path.basename(p).startswith(("config_", "refrun_")))
 
 
 def _load(path):
