@@ -1471,7 +1471,18 @@ bool launch_stream(const NnlsLaunch& a, cudaStream_t s) {
   if (r <= 10) return launch_stream_rp<10, 2>(a, s);
   if (r <= 12) return launch_stream_rp<12, 4>(a, s);
   if (r <= 16) return launch_stream_rp<16, 4>(a, s);
-  if (r <= 20) return launch_stream_rp<20, 4>(a, s);
+  if (r <= 20) {
+    // window length (terms every lane adds itself) of the r = 20 plan: 3 (r02ak sweep at C2:
+    // L = 3 4372, 4 4336, 5 4333, 6 4263 iters/s); NTF_NNLS_L overrides
+    static const int lwin = [] {
+      const char* e = std::getenv("NTF_NNLS_L");
+      return e ? std::atoi(e) : 3;
+    }();
+    if (lwin == 3 && launch_stream_q<20, 4, 3>(a, s)) return true;
+    if (lwin == 5 && launch_stream_q<20, 4, 5>(a, s)) return true;
+    if (lwin == 6 && launch_stream_q<20, 4, 6>(a, s)) return true;
+    return launch_stream_rp<20, 4>(a, s);
+  }
   if (r <= 24) return launch_stream_rp<24, 8>(a, s);
   if (r <= 32) return launch_stream_rp<32, 8>(a, s);
   return false;

@@ -326,3 +326,49 @@ def test_production_path_is_bitwise_deterministic(P, shape, rank, dtype):
     for a, b in zip(ma, mb):
         assert np.array_equal(a, b)
     prov.close()
+
+
+@pytest.mark.gpu
+def test_async_upload_from_pinned_memory_matches_the_blocking_upload(P):
+    """ntf_tensor_upload_async (what GpuDenseProvider uses for host arrays):
+    the run starts while the tensor is still in flight from pinned memory --
+    session setup and graph capture overlap the copy, every consumer is
+    ordered after it on the device -- and gives bit for bit the trace, factors
+    and ||T||^2 of the blocking ntf_tensor_upload path."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2001_04321_b200 import _lib as L
+    shape, rank = [200, 160, 120], 20
+    spec = P.SyntheticSpec(shape=shape, rank=rank, noise_sigma=0.01, seed=77)
+    t, _ = P.generate(spec)
+    init = P.random_init(shape, rank, P.stream_seed(77, 1))
+    pinned = torch.empty(shape, dtype=torch.float64, pin_memory=True)
+    host = pinned.numpy()
+    np.copyto(host, t)
+    cfg = P.AoConfig(max_outer_iters=12)
+    runs = []
+    for _ in range(2):  # the asynchronous path, run immediately after the enqueue
+        prov = P.GpuDenseProvider(host)
+        model, trace = P.her_run(prov, init, cfg, P.HerParams())
+        runs.append((model, trace, prov.norm_sq()))
+        prov.wait()
+        prov.close()
+    # the blocking C entry point
+    ctx = P.default_context()
+    h = C.c_void_p()
+    arr = (C.c_int64 * 3)(*shape)
+    assert L.lib().ntf_tensor_upload(ctx.handle, host.ctypes.data_as(C.c_void_p), L.NTF_DTYPE_F64, 3, arr, C.byref(h)) == 0
+    prov = P.GpuDenseProvider.__new__(P.GpuDenseProvider)
+    prov.ctx, prov.handle, prov._shape, prov.dtype, prov._source = ctx, h, list(shape), np.float64, host
+    model, trace = P.her_run(prov, init, cfg, P.HerParams())
+    nsq = prov.norm_sq()
+    prov.close()
+    for m2, t2, n2 in runs:
+        assert n2 == nsq
+        assert t2.f0 == trace.f0
+        assert [r.f for r in t2.records] == [r.f for r in trace.records]
+        assert [r.restarted for r in t2.records] == [r.restarted for r in trace.records]
+        for a, b in zip(m2, model):
+            assert np.array_equal(a, b)
