@@ -207,6 +207,10 @@ int ntf_tensor_upload_async(ntf_ctx* ctx, const void* host, int dtype, int order
                             ntf_tensor** out);
 /* Blocks until the upload of `t` (and its ||T||^2) has completed. */
 int ntf_tensor_wait(const ntf_tensor* t);
+/* Page-locked host memory for ntf_tensor_upload_async (cudaHostAlloc /
+ * cudaFreeHost), so a host program needs no CUDA headers of its own. */
+int ntf_pinned_alloc(size_t bytes, void** out);
+int ntf_pinned_free(void* p);
 /* Same, from a device buffer of this context's GPU (copied). Ordering: the
  * copy runs on the context's own stream, so the caller's producer work must
  * be complete -- this entry point synchronises the device before copying.

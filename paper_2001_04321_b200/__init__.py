@@ -14,7 +14,7 @@ from .api import (  # noqa: E402,F401
     RUN_DIMTREE, RUN_DIRECT, RUN_GENERIC, RUN_NO_GRAPH, RUN_NO_OVERLAP, AoConfig, Context, CudaError, GpuDenseProvider, HerIterationInfo, HerParams, HerState, InnerStop,
     InvalidArgument, KruskalModel, LogicError, NcclError, NnlsSolver, ObjectiveProvider, RunTrace, Session,
     SyntheticSpec, TraceRecord, UnsupportedError, ahals_solve, ao_run, default_context, device_count,
-    factor_error, generate, her_run, load_tensor, mttkrp_bytes, mttkrp_flops, nnls_solver_from_name, ntft_info,
+    factor_error, generate, her_run, load_tensor, pinned_empty, mttkrp_bytes, mttkrp_flops, nnls_solver_from_name, ntft_info,
     random_init, save_tensor, TuckerFormat, TuckerProvider, ttm, hosvd_compress, expand,
     slab_range, solve_nnls, stream_seed, update_betas,
 )

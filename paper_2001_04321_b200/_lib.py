@@ -91,6 +91,8 @@ SIGNATURES = {
     "ntf_tensor_upload": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, i64ptr, C.POINTER(C.c_void_p)]),
     "ntf_tensor_upload_async": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, i64ptr, C.POINTER(C.c_void_p)]),
     "ntf_tensor_wait": (C.c_int, [C.c_void_p]),
+    "ntf_pinned_alloc": (C.c_int, [C.c_size_t, C.POINTER(C.c_void_p)]),
+    "ntf_pinned_free": (C.c_int, [C.c_void_p]),
     "ntf_tensor_upload_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, i64ptr,
                                            C.POINTER(C.c_void_p)]),
     "ntf_tensor_upload_device_async": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, i64ptr, C.c_void_p,

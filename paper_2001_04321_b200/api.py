@@ -442,6 +442,21 @@ class ObjectiveProvider:
         raise NotImplementedError
 
 
+def pinned_empty(shape, dtype=np.float64):
+    """A numpy array in page-locked host memory (ntf_pinned_alloc): uploads
+    from it run at link speed and overlap the solver's setup
+    (ntf_tensor_upload_async). Freed when the array is garbage-collected."""
+    import weakref
+    dtype = np.dtype(dtype)
+    n = int(np.prod(shape)) * dtype.itemsize
+    p = C.c_void_p()
+    _check(L.lib().ntf_pinned_alloc(n, C.byref(p)))
+    buf = (C.c_char * max(n, 1)).from_address(p.value)
+    arr = np.frombuffer(buf, dtype=dtype, count=int(np.prod(shape))).reshape(shape)
+    weakref.finalize(buf, L.lib().ntf_pinned_free, p)
+    return arr
+
+
 class GpuDenseProvider(ObjectiveProvider):
     """DenseProvider (provider.hpp:22-34) backed by a device-resident tensor.
 

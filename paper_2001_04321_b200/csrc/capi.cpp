@@ -512,6 +512,19 @@ int ntf_tensor_wait(const ntf_tensor* t) {
   });
 }
 
+int ntf_pinned_alloc(size_t bytes, void** out) {
+  return guarded([&] {
+    need(out, "out");
+    NTF_CUDA(cudaHostAlloc(out, bytes ? bytes : 1, cudaHostAllocDefault));
+  });
+}
+
+int ntf_pinned_free(void* p) {
+  return guarded([&] {
+    if (p) NTF_CUDA(cudaFreeHost(p));
+  });
+}
+
 int ntf_tensor_upload_ntft(ntf_ctx* ctx, const char* path, int dtype, ntf_tensor** out) {
   return guarded([&] {
     need(out, "out");

@@ -337,15 +337,12 @@ def test_async_upload_from_pinned_memory_matches_the_blocking_upload(P):
     and ||T||^2 of the blocking ntf_tensor_upload path."""
     import ctypes as C
 
-    import torch
-
     from paper_2001_04321_b200 import _lib as L
     shape, rank = [200, 160, 120], 20
     spec = P.SyntheticSpec(shape=shape, rank=rank, noise_sigma=0.01, seed=77)
     t, _ = P.generate(spec)
     init = P.random_init(shape, rank, P.stream_seed(77, 1))
-    pinned = torch.empty(shape, dtype=torch.float64, pin_memory=True)
-    host = pinned.numpy()
+    host = P.pinned_empty(shape, np.float64)  # ntf_pinned_alloc: page-locked, so the copy is truly asynchronous
     np.copyto(host, t)
     cfg = P.AoConfig(max_outer_iters=12)
     runs = []

@@ -1,0 +1,115 @@
+"""GPU parity against THE REFERENCE ITSELF (not the restatement).
+
+`oracle/_ref/libntf_ref.so` is the reference's own unmodified sources built by
+`oracle/ref_build/` (Eigen stand-in; the reference's unit suites pass over it,
+tests/test_ref_build.py). It is built where /root/reference exists and travels
+to the GPU box as a prebuilt file; these tests put the sm_100a path (through
+the C ABI) directly beside it with the bars of tests/parity.py: per-call MTTKRP
+1e-12, AHALS 1e-12 with identical sweep counts, 50-iteration HER / AO traces
+with identical restart decisions and beta_k, final factors, e_k. They skip
+(loudly) only when no reference build is present.
+"""
+import numpy as np
+import pytest
+
+import pyref
+from parity import compare_traces, rel_fro
+
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not pyref.available(), reason="oracle/_ref/libntf_ref.so is absent")]
+
+
+@pytest.fixture(scope="module")
+def R():
+    assert pyref.is_reference_build()
+    return pyref
+
+
+@pytest.mark.parametrize("shape,rank", [([50, 50, 50], 10), ([37, 41, 29], 20), ([20, 21, 22, 23], 16),
+                                        ([300, 30, 30], 20), ([64, 48, 40], 20), ([40, 30, 20], 32), ([16, 9], 4)])
+def test_mttkrp_vs_reference(P, R, shape, rank):
+    """ntf::mttkrp (kernels.cpp:161-191) and the reference's own serial oracle
+    ntf::ref::mttkrp (reference.cpp:89-99)."""
+    gen = np.random.default_rng(sum(shape) + rank)
+    t = gen.random(shape)
+    m = [gen.random((d, rank)) for d in shape]
+    prov = P.GpuDenseProvider(t)
+    assert abs(prov.norm_sq() - R.norm_sq(t)) <= 1e-13 * R.norm_sq(t)
+    for mode in range(len(shape)):
+        got = prov.mttkrp(m, mode)
+        assert rel_fro(got, R.mttkrp(t, m, mode)) < 1e-12
+        if t.size <= 50 ** 3:
+            assert rel_fro(got, R.ref_mttkrp(t, m, mode)) < 1e-12
+    prov.close()
+
+
+@pytest.mark.parametrize("rows,r", [(6, 3), (300, 20), (500, 32), (100, 16), (1100, 10)])
+def test_ahals_vs_reference(P, R, rows, r):
+    """ahals_solve (nnls.cpp:15-49): the same iterate, the same sweep count."""
+    gen = np.random.default_rng(rows + r)
+    b = gen.random((rows + 50, r))
+    g = b.T @ b
+    c = gen.random((rows, r)) * r
+    w0 = gen.random((rows, r))
+    for max_iters, tol in ((50, 1e-2), (7, 1e-9)):
+        want, sweeps = R.ahals_solve(g, c, w0, max_iters, tol, return_sweeps=True)
+        got, got_sweeps = P.ahals_solve(g, c, w0, P.InnerStop(max_iters, tol), return_sweeps=True)
+        assert got_sweeps == sweeps
+        assert rel_fro(got, want) < 1e-12
+
+
+@pytest.mark.parametrize("solver", ["pgd", "nesterov", "admm", "active_set"])
+def test_other_solvers_vs_reference(P, R, solver):
+    gen = np.random.default_rng(5)
+    rows, r = 120, 8
+    b = gen.random((rows + 30, r))
+    g = b.T @ b
+    c = gen.random((rows, r)) * r
+    w0 = gen.random((rows, r))
+    want = R.solve_nnls(solver, g, c, w0, 30, 1e-3)
+    got = P.solve_nnls(P.nnls_solver_from_name(solver), g, c, w0, P.InnerStop(30, 1e-3))
+    assert rel_fro(got, want) < 1e-9
+
+
+RUNS = [([50, 50, 50], 10, 0.01, 101, False),  # BASELINE config 1
+        ([30, 30, 30], 5, 0.0, 4000, False), ([20, 20, 20, 20], 4, 0.01, 103, False),
+        ([64, 48, 40], 20, 0.01, 12, False),  # the smoke shape: stream-K / fast kernels, r = 20 NNLS plan
+        ([15, 12, 10], 4, 0.001, 97, True)]
+
+
+@pytest.mark.parametrize("shape,rank,sigma,seed,ill", RUNS)
+@pytest.mark.parametrize("algo", ["her", "ao"])
+def test_traces_vs_reference(P, R, algo, shape, rank, sigma, seed, ill):
+    """her_run (her.cpp:40-110) / ao_run (ao.cpp:17-52) by the reference itself
+    against the production path (dimension tree, graph replay): f0, 50 x f_k,
+    every restart decision and beta_k, final factors, e_50."""
+    spec = P.SyntheticSpec(shape=shape, rank=rank, noise_sigma=sigma, seed=seed, ill_conditioned=ill)
+    t, truth = P.generate(spec)
+    tr, truth_r = R.generate(shape, rank, sigma, ill, seed)
+    assert np.array_equal(np.asarray(t), tr)  # the host generator against the reference's, bit for bit
+    assert all(np.array_equal(a, b) for a, b in zip(truth.factors, truth_r))
+    init = P.random_init(shape, rank, P.stream_seed(seed, 1))
+    fr, f0, recs = R.run(algo, tr, init.factors, max_outer_iters=50, truth=truth_r)
+    cfg = P.AoConfig(max_outer_iters=50)
+    if algo == "her":
+        model, trace = P.her_run(t, init, cfg, P.HerParams())
+    else:
+        model, trace = P.ao_run(t, init, cfg)
+    stats = compare_traces(trace, f0, recs, R.norm_sq(tr), check_restarts=(algo == "her"))
+    assert stats["checked"] == 50
+    for a, b in zip(model, fr):
+        assert rel_fro(a, b) < 1e-6
+    assert abs(P.factor_error(model, truth) - recs[-1]["e"]) <= 1e-6
+
+
+def test_tucker_provider_vs_reference(P, R):
+    """compressed_mttkrp (tucker.cpp:62-77)."""
+    gen = np.random.default_rng(23)
+    full, ranks, r = [24, 20, 18], [6, 5, 4], 5
+    core = gen.random(ranks)
+    bases = [np.linalg.qr(gen.standard_normal((d, k)))[0] for d, k in zip(full, ranks)]
+    m = [gen.random((d, r)) for d in full]
+    prov = P.TuckerProvider(P.TuckerFormat(core, bases))
+    for mode in range(3):
+        assert rel_fro(prov.mttkrp(m, mode), R.compressed_mttkrp(core, bases, m, mode)) < 1e-11
+    prov.close()
