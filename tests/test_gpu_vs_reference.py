@@ -113,3 +113,38 @@ def test_tucker_provider_vs_reference(P, R):
     for mode in range(3):
         assert rel_fro(prov.mttkrp(m, mode), R.compressed_mttkrp(core, bases, m, mode)) < 1e-11
     prov.close()
+
+
+@pytest.mark.parametrize("shape,rank,seed", [([64, 48, 40], 20, 12), ([96, 80, 72], 32, 31)])
+def test_fp32_tensor_traces_vs_reference(P, R, shape, rank, seed):
+    """An FP32 data set (BASELINE configs 4/5): the reference stores doubles,
+    so it runs on the float values widened exactly; the GPU multiplies in FP32
+    with FP32 factor mirrors and FP64 accumulation of short FP32 sums (per-call
+    bar 1e-5). Bars as tests/test_config_parity.py uses at config 4: f_k within
+    1e-6 ||T||^2, restart decisions identical wherever |F_k - F_{k-1}| exceeds
+    4e-6 ||T||^2, final factors 1e-3, e_k 1e-2 relative + 1e-4 (e_50 is a few
+    1e-3 on these well-conditioned instances, where FP32 products move it by
+    a few 1e-5)."""
+    spec = P.SyntheticSpec(shape=shape, rank=rank, noise_sigma=0.01, seed=seed)
+    t64, truth = P.generate(spec)
+    t = np.asarray(t64, np.float32)
+    init = P.random_init(shape, rank, P.stream_seed(seed, 1))
+    fr, f0, recs = R.run("her", t, init.factors, max_outer_iters=50, truth=truth.factors)
+    nsq = R.norm_sq(t)
+    prov = P.GpuDenseProvider(t)
+    for mode in range(len(shape)):
+        assert rel_fro(prov.mttkrp(init, mode), R.mttkrp(t, init.factors, mode)) < 1e-5
+    model, trace = P.her_run(prov, init, P.AoConfig(max_outer_iters=50), P.HerParams())
+    prov.close()
+    assert abs(trace.f0 - f0) <= 1e-6 * nsq
+    prev, decided = f0, 0
+    for rec, want in zip(trace.records, recs):
+        assert abs(rec.f - want["f"]) <= 1e-6 * nsq, (rec, want)
+        if abs(want["f"] - prev) > 4e-6 * nsq:
+            decided += 1
+            assert rec.restarted == want["restarted"]
+        prev = want["f"]
+    assert decided >= 10
+    for a, b in zip(model, fr):
+        assert rel_fro(a, b) < 1e-3
+    assert abs(P.factor_error(model, truth) - recs[-1]["e"]) <= 1e-2 * recs[-1]["e"] + 1e-4
