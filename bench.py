@@ -215,6 +215,30 @@ def cpu_mttkrp_times(cfg_name, threads, reps=5):
     return out
 
 
+def reference_build_sample(cfg_name, algo, budget_s=4.0):
+    """The reference's OWN sources (oracle/_ref/libntf_ref.so, built against
+    the Eigen stand-in) on a bounded sample of the same instance: reported
+    beside the timed restatement, not instead of it -- the stand-in's
+    temporaries make this build several times slower than a real Eigen build
+    would be, so it is a lower bound of the reference's speed."""
+    try:
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        import pyref
+        if not os.path.exists(pyref.LIB_PATH):
+            return None
+        O, t, init = _oracle_instance(cfg_name)
+        _, _, recs = pyref.run(algo, t, init, max_time_s=budget_s)
+        if len(recs) >= 2:
+            n, secs = len(recs) - 1, recs[-1]["time_s"] - recs[0]["time_s"]
+        else:
+            n, secs = 1, recs[0]["time_s"]
+        return {"value": n / secs, "unit": UNIT, "iterations": n, "seconds": secs,
+                "what": "the reference's unmodified sources built against the Eigen stand-in of oracle/ref_build "
+                        "(a checker: slower than a real Eigen build; lower bound of the reference's speed)"}
+    except Exception as exc:  # the checker is optional here
+        return {"unavailable": f"{type(exc).__name__}: {exc}"}
+
+
 def run_reference_arm(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -226,6 +250,7 @@ def run_reference_arm(args):
         return
     rate, secs = cpu_reference(args.config, args.algo, args.steps, args.warmup, threads=cores)
     shape, r, sigma, dt, seed, idx, _ = CONFIGS[args.config]
+    ref_build = reference_build_sample(args.config, args.algo)
     line = {
         "impl": "reference", "metric": metric_name(args.algo), "value": rate, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps,
@@ -240,6 +265,8 @@ def run_reference_arm(args):
                                    "fair timing target"},
         "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    if ref_build:
+        line["cpu_baseline"]["reference_build"] = ref_build
     print(json.dumps(line), flush=True)
 
 
