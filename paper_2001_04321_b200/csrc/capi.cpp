@@ -131,6 +131,7 @@ ntf_tensor* make_tensor_with(ntf_ctx* ctx, int dtype, int order, const int64_t* 
   need(shape, "shape");
   if (dtype != NTF_DTYPE_F64 && dtype != NTF_DTYPE_F32) throw InvalidArgument("unknown dtype");
   if (order < 1 || order > NTF_MAX_ORDER) throw InvalidArgument("tensor order must lie in 1..8");
+  NvtxRange nvtx("ntf:upload");
   auto* t = new ntf_tensor();
   try {
     t->ctx = ctx;
@@ -250,6 +251,7 @@ void run_driver(int algo, ntf_ctx* ctx, const ntf_tensor* t, const double* init,
     validate_params(*params);
   }
   check_run_inputs(t, init, rank, *cfg);
+  NvtxRange nvtx(algo == 0 ? "ntf:her_run" : "ntf:ao_run");
   const auto shape = int_shape(t);
   // NTF_TIMING=1: host-side phase times of the driver on stderr (diagnostics)
   static const bool timing = std::getenv("NTF_TIMING") != nullptr;

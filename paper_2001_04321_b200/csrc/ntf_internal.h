@@ -3,12 +3,33 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>  // header-only; a no-op unless a profiler injects itself
 
 #include <cstdint>
+#include <cstdio>
 #include <stdexcept>
 #include <string>
 
 #include "../../include/ntf_b200.h"
+
+namespace ntfb {
+
+// NVTX range for the host-side phases (per-mode / per-kernel
+// ranges for ncu / Nsight timelines): "ntf:upload", "ntf:session", "ntf:mttkrp m",
+// "ntf:nnls m", "ntf:graph", "ntf:run".
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  NvtxRange(const char* name, int mode) {
+    char buf[48];
+    snprintf(buf, sizeof buf, "%s %d", name, mode);
+    nvtxRangePushA(buf);
+  }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
+}  // namespace ntfb
 
 namespace ntfb {
 

@@ -441,6 +441,7 @@ Session::Session(ntf_ctx* ctx, const ntf_tensor* t, int algo, const double* init
   static const bool timing = std::getenv("NTF_TIMING") != nullptr;
   const auto now = [] { return std::chrono::steady_clock::now(); };
   const auto t0 = now();
+  NvtxRange nvtx("ntf:session");
   NTF_CUDA(cudaSetDevice(ctx->device));
   NTF_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
   for (int i = 0; i < order_; ++i) {
@@ -555,7 +556,11 @@ void Session::enqueue_iteration(bool timed) {
       ev_.push_back(e1);
       ev_mode_.push_back(i);
     }
-    eng_->run(i, dF, C_.as<double>(), stream_, e0, e1);
+    {
+      NvtxRange nvtx("ntf:mttkrp", i);
+      eng_->run(i, dF, C_.as<double>(), stream_, e0, e1);
+    }
+    NvtxRange nvtx_nnls("ntf:nnls", i);
     NnlsLaunch a{};
     a.mode = i;
     a.order = order_;
@@ -606,6 +611,7 @@ void Session::enqueue_iteration(bool timed) {
 
 void Session::build_graph() {
   if (exec_ || graph_failed_) return;
+  NvtxRange nvtx("ntf:graph");
   cudaStreamCaptureStatus cs;
   NTF_CUDA(cudaStreamIsCapturing(stream_, &cs));
   if (cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
