@@ -890,7 +890,15 @@ int ntf_session_create(ntf_ctx* ctx, const ntf_tensor* t, int algo, const double
       validate_params(*params);
     }
     check_run_inputs(t, init, rank, *cfg);
-    *out = reinterpret_cast<ntf_session*>(new Session(ctx, t, algo, init, rank, *cfg, params));
+    auto* sess = new Session(ctx, t, algo, init, rank, *cfg, params);
+    try {
+      sess->sync();  // `init` (possibly pinned) has been consumed and setup errors surface here;
+                     // the drivers (ntf_her_run / ntf_ao_run) skip this to overlap an asynchronous upload
+    } catch (...) {
+      delete sess;
+      throw;
+    }
+    *out = reinterpret_cast<ntf_session*>(sess);
   });
 }
 
