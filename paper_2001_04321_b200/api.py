@@ -808,6 +808,15 @@ def _check_inputs(p: GpuDenseProvider, init: KruskalModel, cfg: AoConfig):
             raise InvalidArgument("ground truth does not match the initial model")
 
 
+def _trace_cap(cfg: AoConfig) -> int:
+    """Host trace records to allocate: the iteration budget, or, under a time
+    budget alone, room for 50 000 iterations per second of budget (more than
+    ten times what the device sustains) up to the device-side cap of 2^20."""
+    if cfg.max_outer_iters > 0:
+        return cfg.max_outer_iters
+    return int(min(1 << 20, max(4096, cfg.max_time_s * 50000)))
+
+
 def her_run(data, init, cfg: AoConfig, params: HerParams = None,
             observer: Optional[Callable[[HerIterationInfo], None]] = None, ctx: Optional[Context] = None):
     """her_run (her.hpp:63-69): returns (accepted KruskalModel, RunTrace)."""
@@ -821,7 +830,7 @@ def her_run(data, init, cfg: AoConfig, params: HerParams = None,
     shape, rank = p.shape(), init.rank()
     flat = init.flat()
     out = np.empty_like(flat)
-    cap = cfg.max_outer_iters if cfg.max_outer_iters > 0 else 1 << 20
+    cap = _trace_cap(cfg)
     recs = (L.TraceRecordC * cap)()
     f0 = C.c_double()
     n = C.c_int()
@@ -855,7 +864,7 @@ def ao_run(data, init, cfg: AoConfig, ctx: Optional[Context] = None):
     shape, rank = p.shape(), init.rank()
     flat = init.flat()
     out = np.empty_like(flat)
-    cap = cfg.max_outer_iters if cfg.max_outer_iters > 0 else 1 << 20
+    cap = _trace_cap(cfg)
     recs = (L.TraceRecordC * cap)()
     f0 = C.c_double()
     n = C.c_int()

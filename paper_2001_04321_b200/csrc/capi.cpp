@@ -261,9 +261,21 @@ void run_driver(int algo, ntf_ctx* ctx, const ntf_tensor* t, const double* init,
   Session s(ctx, t, algo, init, rank, *cfg, params);
   const auto t1 = now();
   const long long len = model_len(t, rank);
-  const bool per_iteration = observer != nullptr || cfg->record_factor_error || cfg->max_time_s > 0.0;
+  const bool per_iteration = observer != nullptr || cfg->record_factor_error;
   std::vector<double> e_values;
-  if (!per_iteration) {
+  if (!per_iteration && cfg->max_time_s > 0.0) {
+    // A time budget alone: the device decides (the last block's kernel sets
+    // `done` once the run clock passes the budget, her.cpp:105 / ao.cpp:48,
+    // and every later kernel of the run is a no-op that writes no record), so
+    // the host only has to stop enqueuing: graph replays in batches of 8
+    // with one synchronisation per batch instead of one per iteration.
+    const int batch = 8;
+    for (;;) {
+      s.step(batch);
+      s.sync();
+      if (s.done()) break;
+    }
+  } else if (!per_iteration) {
     s.step(cfg->max_outer_iters);
     const auto t2 = now();
     s.sync();
