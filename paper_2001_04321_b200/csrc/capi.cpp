@@ -95,14 +95,17 @@ void check_run_inputs(const ntf_tensor* t, const double* init, int rank, const n
   if (cfg.solver == NTF_SOLVER_ACTIVE_SET && rank > 32)
     throw Unsupported("the GPU active-set solver serves ranks up to 32");
   if (cfg.inner_stop.max_iters < 0) throw InvalidArgument("inner max_iters must be >= 0");
-  // the fused block update keeps a factor on one thread-block cluster
-  // (launch_nnls): refuse up front, before the session is built
-  if (rank > kMaxRank) throw Unsupported("rank above the fused NNLS kernel's limit (64)");
-  for (int i = 0; i < t->order; ++i)
-    if (t->shape[i] > kMaxNnlsRows)
-      throw Unsupported("mode " + std::to_string(i) + " has " + std::to_string(t->shape[i]) +
-                        " rows; the fused NNLS kernel holds at most " + std::to_string(kMaxNnlsRows) +
-                        " rows per factor");
+  // limits are refused up front, before the session is built. AHALS serves
+  // any factor height (taller than one cluster: the grid-kernel path of
+  // kernels_nnls_tall.cu); the other inner solvers keep a factor on one
+  // thread-block cluster
+  if (rank > kMaxRank) throw Unsupported("rank above the NNLS kernels' limit (64)");
+  if (cfg.solver != NTF_SOLVER_AHALS)
+    for (int i = 0; i < t->order; ++i)
+      if (t->shape[i] > kMaxNnlsRows)
+        throw Unsupported("mode " + std::to_string(i) + " has " + std::to_string(t->shape[i]) +
+                          " rows; the " + "PGD / Nesterov / ADMM / active-set kernels hold at most " +
+                          std::to_string(kMaxNnlsRows) + " rows per factor (AHALS has no such limit)");
 }
 
 // The tensor handle of this rank's mode-1 slab; `fill` copies the slab's
@@ -848,8 +851,12 @@ int ntf_solve_nnls(ntf_ctx* ctx, int solver, const double* gram, const double* t
     a.max_iters = st.max_iters;
     a.tol = st.rel_change_tol;
     a.scratch = scratch.as<double>();
-    DevBuf work, err;
+    DevBuf work, err, tall;
     if (solver == NTF_SOLVER_AHALS) {
+      if (nnls_needs_tall(rows, rank)) {
+        tall = DevBuf(nnls_tall_workspace(rows, rank) * sizeof(double));
+        a.tall = tall.as<double>();
+      }
       launch_nnls(a, ctx->stream);
     } else {
       work = DevBuf(2 * n * 8);

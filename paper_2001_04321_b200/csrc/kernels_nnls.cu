@@ -1499,9 +1499,23 @@ void nnls_prof_read(unsigned long long out[8 + 384], bool reset) {
   }
 }
 
+// One cluster holds at most 4096 rows (one lane per row, 16 CTAs x 256); the spilling plans of
+// r > 32 at most 2048. NTF_NNLS_TALL=1 sends every update through the tall path (tests).
+bool nnls_needs_tall(int rows, int rank) {
+  static const bool force = [] {
+    const char* e = std::getenv("NTF_NNLS_TALL");
+    return e && std::atoi(e) != 0;
+  }();
+  return force || rows > kMaxNnlsRows || (rank > 32 && rows > 2048);
+}
+
 void launch_nnls(const NnlsLaunch& a, cudaStream_t s) {
   const int r = a.rank;
   if (r < 1 || r > kMaxRank) throw Unsupported("rank outside the fused NNLS kernel's range (1..64)");
+  if (nnls_needs_tall(a.rows, r)) {
+    if (!a.tall) throw Unsupported("factor taller than one cluster holds and no tall-path workspace");
+    return launch_nnls_tall(a, s, a.zero_sweeps ? 0 : a.max_iters);
+  }
   if (launch_stream(a, s)) return;
   if (a.rows > kMaxNnlsRows) throw Unsupported("factor taller than 4096 rows");
   if (r <= 4) return launch_rp<4, 256>(a, s);

@@ -197,8 +197,15 @@ struct NnlsLaunch {
   int solver;        // NTF_SOLVER_* (launch_nnls_solver)
   double* work;      // solver: >= 3 * rows * rank doubles of per-row state
   int* error;        // solver: first failure code (0 = none), see solver_error_message
+  // workspace of the tall-factor path (kernels_nnls_tall.cu): >= nnls_tall_workspace(rows, rank)
+  // doubles, or null (factors beyond one cluster are then refused)
+  double* tall;
 };
 void launch_nnls(const NnlsLaunch& a, cudaStream_t s);
+// Factors too tall for one cluster (or NTF_NNLS_TALL=1): the same update as plain grid kernels.
+size_t nnls_tall_workspace(int rows, int rank);
+void launch_nnls_tall(const NnlsLaunch& a, cudaStream_t s, int max_iters_host);
+bool nnls_needs_tall(int rows, int rank);
 // PGD / Nesterov / ADMM / active-set (nnls.cpp:51-211) on one thread-block
 // cluster: reads G (Hadamard of the other modes' X-role Grams, or gram_in),
 // C and the warm start (X, or w0), writes the result rows to w_out.

@@ -467,6 +467,12 @@ Session::Session(ntf_ctx* ctx, const ntf_tensor* t, int algo, const double* init
     solve_work_ = DevBuf(2 * size_t(maxrows) * rank * sizeof(double));
   }
   dF_ = DevBuf(sizeof(DevFactors));
+  {  // factors beyond one cluster (or NTF_NNLS_TALL=1): workspace of the grid-kernel block update
+    size_t need_tall = 0;
+    for (int i = 0; i < order_; ++i)
+      if (nnls_needs_tall(rows_[i], rank)) need_tall = std::max(need_tall, nnls_tall_workspace(rows_[i], rank));
+    if (need_tall) tall_work_ = DevBuf(need_tall * sizeof(double));
+  }
 
   std::memset(&hF_, 0, sizeof hF_);
   hF_.order = order_;
@@ -575,6 +581,8 @@ void Session::enqueue_iteration(bool timed) {
     a.scratch = scratch_.as<double>();
     a.bufs = hF_;
     a.has_bufs = 1;
+    a.max_iters = cfg_.inner_stop.max_iters;  // the host's copy (launch count of the tall path's sweeps)
+    a.tall = tall_work_.p ? tall_work_.as<double>() : nullptr;
     if (cfg_.solver != NTF_SOLVER_AHALS) {  // solve_nnls (nnls.cpp:213-222), then the fused epilogue
       NnlsLaunch b = a;
       b.solver = cfg_.solver;

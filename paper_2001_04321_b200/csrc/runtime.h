@@ -207,6 +207,7 @@ class Session {
   DevFactors hF_{};
   DevBuf dF_, fac_, fac32_, grams_, C_, state_, trace_, scratch_, counter_;
   DevBuf solve_buf_, solve_work_;  // another inner solver: its result rows and per-row state
+  DevBuf tall_work_;               // block update of factors beyond one cluster (kernels_nnls_tall.cu)
   DevBuf init_scratch_;            // partial Grams of the constructor's setup kernels (kept: no host sync there)
   int trace_cap_ = 0;
   cudaGraph_t graph_ = nullptr;

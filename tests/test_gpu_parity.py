@@ -296,12 +296,59 @@ def test_driver_validation(P):
         P.her_run(t, init, P.AoConfig(solver=7, max_outer_iters=3))
 
 
-def test_too_tall_factor_is_refused_up_front(P):
-    """The fused block update holds a factor on one 16-CTA cluster (4096 rows,
-    r <= 64): such runs fail before the session is built (ntf_her_run)."""
+@pytest.mark.parametrize("shape,rank,seed", [([5000, 6, 5], 3, 1), ([9, 4500, 7], 4, 2), ([6, 5, 4100], 2, 3)])
+@pytest.mark.parametrize("algo", ["her", "ao"])
+def test_factors_taller_than_one_cluster(P, oracle, algo, shape, rank, seed):
+    """The reference has no factor-height limit (nnls.cpp:15-49 loops over all
+    rows). A mode beyond one 16-CTA cluster (4096 rows) takes the grid-kernel
+    block update (kernels_nnls_tall.cu) -- first, middle or last mode -- with
+    the same trace, decisions, factors and e_k as the oracle."""
+    t, truth, init = _instance(P, shape, rank, 0.01, seed)
+    cfg = P.AoConfig(max_outer_iters=12)
+    if algo == "her":
+        model, trace = P.her_run(t, init, cfg, P.HerParams())
+    else:
+        model, trace = P.ao_run(t, init, cfg)
+    fo, f0, recs = oracle.run(algo, t, init.factors, max_outer_iters=12)
+    stats = compare_traces(trace, f0, recs, oracle.norm_sq(t), n_check=12, check_restarts=(algo == "her"))
+    assert stats["checked"] == 12
+    for a, b in zip(model, fo):
+        assert rel_fro(a, b) < 1e-6
+    assert abs(P.factor_error(model, truth) - oracle.factor_error(fo, truth.factors)) <= 1e-6
+
+
+def test_tall_standalone_ahals_and_solver_limits(P, oracle):
+    """ntf_solve_nnls on 6000 rows: the same iterate and sweep count as the
+    oracle; the other inner solvers still refuse factors beyond one cluster."""
+    gen = np.random.default_rng(11)
+    rows, r = 6000, 8
+    b = gen.random((rows // 10, r))
+    g = b.T @ b
+    c = gen.random((rows, r)) * r
+    w0 = gen.random((rows, r))
+    for max_iters, tol in ((50, 1e-2), (5, 0.0)):
+        want, sweeps = oracle.ahals_solve(g, c, w0, max_iters, tol, return_sweeps=True)
+        got, got_sweeps = P.ahals_solve(g, c, w0, P.InnerStop(max_iters, tol), return_sweeps=True)
+        assert got_sweeps == sweeps
+        assert rel_fro(got, want) < 1e-12
     t, _, init = _instance(P, [5000, 2, 2], 1, 0.0, 1)
     with pytest.raises(P.UnsupportedError, match="4096"):
-        P.her_run(t, init, P.AoConfig(max_outer_iters=2))
+        P.her_run(t, init, P.AoConfig(max_outer_iters=2, solver=P.NnlsSolver.pgd))
+
+
+def test_tall_path_forced_on_small_instances_matches_the_fused_kernels():
+    """NTF_NNLS_TALL=1 routes every block update through the grid-kernel path:
+    the trace and AHALS parity tests of this module, re-run that way in a
+    child process (the switch is read once per process)."""
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, NTF_NNLS_TALL="1")
+    here = os.path.dirname(os.path.abspath(__file__))
+    out = subprocess.run([sys.executable, "-m", "pytest", os.path.join(here, "test_gpu_parity.py"), "-m", "gpu", "-q",
+                          "-x", "-k", "her_trace_parity or ao_trace_parity or ahals_vs_oracle or bookkeeping"],
+                         env=env, capture_output=True, text=True, timeout=1500)
+    assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-2000:]
 
 
 @pytest.mark.parametrize("shape,rank,dtype", [([120, 100, 80], 20, np.float64), ([40, 36, 34, 32], 16, np.float64),
