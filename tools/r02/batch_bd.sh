@@ -1,7 +1,7 @@
 #!/bin/bash
 # Full ncu captures (--set full) of one outer iteration's kernels at C2, C3, C4;
 # the reports stay on the box (too large), per-launch summaries + raw CSVs come back.
-O=gpurun_out/r02ab; mkdir -p $O
+O=gpurun_out/r02bd; mkdir -p $O
 B="python bench.py --steps 5 --warmup 3 --no-cpu-baseline"
 timeout 300 $B > $O/plain_c2.json 2> $O/plain_c2.err; echo "plain c2 rc=$?"
 for c in c2:16:8 c3:20:10 c4:16:8; do
