@@ -435,6 +435,7 @@ int ntf_ctx_create(int device, ntf_ctx** out) {
       NTF_CUDA(cudaSetDevice(device));
       retain_pool_memory(device);
       NTF_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+      NTF_CUDA(cudaStreamCreateWithFlags(&c->setup, cudaStreamNonBlocking));
       c->sms = device_sm_count();
       c->scratch = DevBuf(4096 * sizeof(double));
     } catch (...) {

@@ -1,3 +1,5 @@
+#include <cstring>
+#include <algorithm>
 // Generic MTTKRP, deterministic reductions, Grams and the cheap objective.
 //
 // Determinism contract (README.md:155-157 of the reference): every value is
@@ -337,6 +339,58 @@ void launch_apply_time_budget(RunState* st, cudaStream_t s) {
 void launch_compact_rows(const double* gathered, long long maxrows, const long long* begins,
                          const long long* counts, int world, int r, double* out, cudaStream_t s) {
   compact_rows_kernel<<<64, 256, 0, s>>>(gathered, maxrows, begins, counts, world, r, out);
+  NTF_CUDA(cudaGetLastError());
+}
+
+
+// ---- small host -> device uploads as kernel parameters --------------------
+// A cudaMemcpy of a small table queues behind whatever the copy engine is
+// doing -- behind the 216 MB tensor upload of an asynchronous ntf_tensor_upload,
+// which would stall session setup for milliseconds. Kernel parameters travel
+// with the launch instead: the payload is cut into chunks that ride in the
+// parameter buffer and a few threads write them out.
+namespace {
+constexpr int kParamChunk = 28672;  // bytes per launch (CUDA 12.1+: 32 764 bytes of kernel parameters on sm_70+)
+struct ParamBlob {
+  unsigned long long w[kParamChunk / 8];
+};
+__global__ void param_upload_kernel(unsigned long long* dst, ParamBlob blob, int n8, unsigned char* tail_dst,
+                                    unsigned long long tail, int tail_n) {
+  for (int i = threadIdx.x; i < n8; i += blockDim.x) dst[i] = blob.w[i];
+  if (threadIdx.x < tail_n) tail_dst[threadIdx.x] = (unsigned char)(tail >> (8 * threadIdx.x));
+}
+}  // namespace
+
+namespace {
+__global__ void zero_kernel(unsigned* dst, size_t n4) {
+  for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n4; i += size_t(gridDim.x) * blockDim.x) dst[i] = 0u;
+}
+}  // namespace
+
+void dev_zero(void* dst, size_t bytes, cudaStream_t s) {
+  if (bytes % 4 || reinterpret_cast<uintptr_t>(dst) % 4) throw LogicError("dev_zero: 4-byte granularity");
+  if (!bytes) return;
+  const size_t n4 = bytes / 4;
+  zero_kernel<<<unsigned(std::min<size_t>(64, (n4 + 255) / 256)), 256, 0, s>>>(static_cast<unsigned*>(dst), n4);
+  NTF_CUDA(cudaGetLastError());
+}
+
+void dev_upload(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  if (reinterpret_cast<uintptr_t>(dst) % 8) throw LogicError("dev_upload: destination must be 8-byte aligned");
+  const unsigned char* p = static_cast<const unsigned char*>(src);
+  unsigned char* d = static_cast<unsigned char*>(dst);
+  size_t off = 0;
+  while (off < bytes) {
+    const size_t n = std::min(bytes - off, size_t(kParamChunk));
+    ParamBlob blob;
+    const int n8 = int(n / 8), tail_n = int(n % 8);
+    std::memcpy(blob.w, p + off, size_t(n8) * 8);
+    unsigned long long tail = 0;
+    if (tail_n) std::memcpy(&tail, p + off + size_t(n8) * 8, size_t(tail_n));
+    param_upload_kernel<<<1, 128, 0, s>>>(reinterpret_cast<unsigned long long*>(d + off), blob, n8,
+                                          d + off + size_t(n8) * 8, tail, tail_n);
+    off += n;
+  }
   NTF_CUDA(cudaGetLastError());
 }
 

@@ -216,5 +216,9 @@ const char* solver_error_message(int code);
 void nnls_prof_read(unsigned long long out[8 + 384], bool reset);
 
 int device_sm_count();
+// Small host -> device upload carried in kernel parameters (no copy engine: it does not queue
+// behind a large transfer in flight); asynchronous on `s`, the host buffer may be reused at once.
+void dev_upload(void* dst, const void* src, size_t bytes, cudaStream_t s);
+void dev_zero(void* dst, size_t bytes, cudaStream_t s);  // zero fill by a kernel (same reason)
 
 }  // namespace ntfb

@@ -17,6 +17,38 @@
 
 namespace ntfb {
 
+// Engine tables: small ones travel as kernel parameters on the context's
+// setup stream (they must not queue behind a tensor upload in flight on the
+// copy engine -- ntf_tensor_upload_async), large ones take the copy engine.
+// Blocking either way: the table is visible to every stream on return.
+static void table_upload(const ntf_ctx* ctx, void* dst, const void* src, size_t bytes) {
+  if (bytes == 0) return;
+  if (bytes <= 2 * 1024 * 1024 && ctx->setup) {
+    static const bool trace = std::getenv("NTF_TIMING_ALLOC") != nullptr;
+    const auto t0 = std::chrono::steady_clock::now();
+    dev_upload(dst, src, bytes, ctx->setup);
+    const auto t1 = std::chrono::steady_clock::now();
+    NTF_CUDA(cudaStreamSynchronize(ctx->setup));
+    if (trace) {
+      const auto t2 = std::chrono::steady_clock::now();
+      fprintf(stderr, "[ntf table] %zu bytes: launch %.2f ms, sync %.2f ms\n", bytes,
+              std::chrono::duration<double, std::milli>(t1 - t0).count(),
+              std::chrono::duration<double, std::milli>(t2 - t1).count());
+    }
+  } else {
+    NTF_CUDA(cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice));
+  }
+}
+
+static void table_zero(const ntf_ctx* ctx, void* dst, size_t bytes) {
+  if (ctx->setup) {
+    dev_zero(dst, bytes, ctx->setup);
+    NTF_CUDA(cudaStreamSynchronize(ctx->setup));
+  } else {
+    NTF_CUDA(cudaMemset(dst, 0, bytes));
+  }
+}
+
 // ---- DevBuf ------------------------------------------------------------------
 // Device buffers come from the device's stream-ordered memory pool, which
 // the context configures to keep freed memory (release threshold = max):
@@ -24,18 +56,42 @@ namespace ntfb {
 // driver unmapping and remapping hundreds of MB (cudaFree of a 216 MB
 // tensor measured 1-800 ms on the B200 boxes). Owners synchronise the
 // streams that used a buffer before it is destroyed.
+// The pool's allocations and frees run on one private non-blocking stream per
+// device. (The legacy default stream served before: synchronising it waited
+// for an asynchronous tensor upload in flight on the context's stream --
+// 3 ms of a session's setup at C2, NTF_TIMING_ALLOC=1 -- although that stream
+// is non-blocking.)
+static cudaStream_t alloc_stream() {
+  static cudaStream_t streams[64] = {};
+  int dev = 0;
+  NTF_CUDA(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 64) return cudaStreamLegacy;
+  if (!streams[dev]) NTF_CUDA(cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking));
+  return streams[dev];
+}
+
 DevBuf::DevBuf(size_t n) : bytes(n) {
   if (n) {
-    NTF_CUDA(cudaMallocAsync(&p, n, cudaStreamLegacy));
-    NTF_CUDA(cudaStreamSynchronize(cudaStreamLegacy));  // usable from any stream
+    static const bool trace = std::getenv("NTF_TIMING_ALLOC") != nullptr;
+    const auto t0 = std::chrono::steady_clock::now();
+    cudaStream_t as = alloc_stream();
+    NTF_CUDA(cudaMallocAsync(&p, n, as));
+    const auto t1 = std::chrono::steady_clock::now();
+    NTF_CUDA(cudaStreamSynchronize(as));  // usable from any stream
+    if (trace) {
+      const auto t2 = std::chrono::steady_clock::now();
+      const double a = std::chrono::duration<double, std::milli>(t1 - t0).count();
+      const double b = std::chrono::duration<double, std::milli>(t2 - t1).count();
+      if (a + b > 0.1) fprintf(stderr, "[ntf alloc] %zu bytes: malloc %.2f ms, sync %.2f ms\n", n, a, b);
+    }
   }
 }
 DevBuf::~DevBuf() {
-  if (p) cudaFreeAsync(p, cudaStreamLegacy);
+  if (p) cudaFreeAsync(p, alloc_stream());
 }
 DevBuf& DevBuf::operator=(DevBuf&& o) noexcept {
   if (this != &o) {
-    if (p) cudaFreeAsync(p, cudaStreamLegacy);
+    if (p) cudaFreeAsync(p, alloc_stream());
     p = o.p;
     bytes = o.bytes;
     o.p = nullptr;
@@ -129,9 +185,9 @@ MttkrpEngine::MttkrpEngine(const ntf_ctx* ctx, const ntf_tensor* t, int rank, un
       core_hF_.rows[l] = td_.ranks[l];
     }
     core_dF_ = DevBuf(sizeof(DevFactors));
-    NTF_CUDA(cudaMemcpy(core_dF_.p, &core_hF_, sizeof core_hF_, cudaMemcpyHostToDevice));
+    table_upload(ctx_, core_dF_.p, &core_hF_, sizeof core_hF_);
     counter_ = DevBuf(2 * sizeof(unsigned));
-    NTF_CUDA(cudaMemset(counter_.p, 0, 2 * sizeof(unsigned)));
+    table_zero(ctx_, counter_.p, 2 * sizeof(unsigned));
     return;
   }
   size_t need = 0;
@@ -207,7 +263,7 @@ MttkrpEngine::MttkrpEngine(const ntf_ctx* ctx, const ntf_tensor* t, int rank, un
       split_ = h;
       ttm_view_ = left_view(h);
       ttm_tab_ = DevBuf(tab.size() * sizeof(int));
-      NTF_CUDA(cudaMemcpy(ttm_tab_.p, tab.data(), tab.size() * sizeof(int), cudaMemcpyHostToDevice));
+      table_upload(ctx_, ttm_tab_.p, tab.data(), tab.size() * sizeof(int));
       ybuf_ = DevBuf(size_t(ttm_view_.I) * rank * sizeof(double));
       need = std::max(need, fast_mttkrp_partial_len(ttm_view_, t->dtype, ctx->sms));
       if (N == 3 && h == N - 1 && !t->rows_only && !(flags & NTF_RUN_NO_OVERLAP)) {
@@ -221,7 +277,7 @@ MttkrpEngine::MttkrpEngine(const ntf_ctx* ctx, const ntf_tensor* t, int rank, un
             p0_sms_ = osms;
             p0_view_ = pv;
             p0_tab_ = DevBuf(ptab.size() * sizeof(int));
-            NTF_CUDA(cudaMemcpy(p0_tab_.p, ptab.data(), ptab.size() * sizeof(int), cudaMemcpyHostToDevice));
+            table_upload(ctx_, p0_tab_.p, ptab.data(), ptab.size() * sizeof(int));
             p0buf_ = DevBuf(size_t(pv.I) * rank * sizeof(double));
             need = std::max(need, fast_mttkrp_partial_len(pv, t->dtype, osms));
           }
@@ -230,7 +286,7 @@ MttkrpEngine::MttkrpEngine(const ntf_ctx* ctx, const ntf_tensor* t, int rank, un
       if (h < N - 1) {
         ttmr_view_ = right_view(h);
         ttmr_tab_ = DevBuf(rtab.size() * sizeof(int));
-        NTF_CUDA(cudaMemcpy(ttmr_tab_.p, rtab.data(), rtab.size() * sizeof(int), cudaMemcpyHostToDevice));
+        table_upload(ctx_, ttmr_tab_.p, rtab.data(), rtab.size() * sizeof(int));
         yrbuf_ = DevBuf(size_t(ttmr_view_.I) * rank * sizeof(double));
         need = std::max(need, fast_mttkrp_partial_len(ttmr_view_, t->dtype, ctx->sms));
       }
@@ -248,16 +304,16 @@ MttkrpEngine::MttkrpEngine(const ntf_ctx* ctx, const ntf_tensor* t, int rank, un
   partial_ = DevBuf(need * sizeof(double));
   if (tree_) {
     tree_arrivals_ = DevBuf(size_t(tree_tiles_max_) * sizeof(unsigned));
-    NTF_CUDA(cudaMemset(tree_arrivals_.p, 0, size_t(tree_tiles_max_) * sizeof(unsigned)));
+    table_zero(ctx_, tree_arrivals_.p, size_t(tree_tiles_max_) * sizeof(unsigned));
   }
   counter_ = DevBuf(2 * sizeof(unsigned));
-  NTF_CUDA(cudaMemset(counter_.p, 0, 2 * sizeof(unsigned)));
+  table_zero(ctx_, counter_.p, 2 * sizeof(unsigned));
   if (!(flags & NTF_RUN_GENERIC))
     for (int m = 0; m < t->order; ++m) {
       const std::vector<int> tab = fast_mttkrp_unit_table(view(m), t->dtype, ctx->sms);
       if (tab.empty()) continue;
       unit_tab_[m] = DevBuf(tab.size() * sizeof(int));
-      NTF_CUDA(cudaMemcpy(unit_tab_[m].p, tab.data(), tab.size() * sizeof(int), cudaMemcpyHostToDevice));
+      table_upload(ctx_, unit_tab_[m].p, tab.data(), tab.size() * sizeof(int));
     }
   if (ctx->comm.active()) {
     const int world = ctx->comm.world;
@@ -271,7 +327,7 @@ MttkrpEngine::MttkrpEngine(const ntf_ctx* ctx, const ntf_tensor* t, int rank, un
     }
     gather_ = DevBuf(size_t(maxrows_) * world * rank * sizeof(double));
     slab_meta_ = DevBuf(meta.size() * sizeof(long long));
-    NTF_CUDA(cudaMemcpy(slab_meta_.p, meta.data(), meta.size() * sizeof(long long), cudaMemcpyHostToDevice));
+    table_upload(ctx_, slab_meta_.p, meta.data(), meta.size() * sizeof(long long));
   }
 }
 
@@ -487,11 +543,17 @@ Session::Session(ntf_ctx* ctx, const ntf_tensor* t, int algo, const double* init
     }
     hF_.sel[i] = 0;
     hF_.rows[i] = rows_[i];
-    NTF_CUDA(cudaMemcpyAsync(hF_.x[i][0], init + off, size_t(n) * sizeof(double), cudaMemcpyHostToDevice, stream_));
-    NTF_CUDA(cudaMemcpyAsync(hF_.x[i][1], init + off, size_t(n) * sizeof(double), cudaMemcpyHostToDevice, stream_));
+    // (kernel-parameter uploads below 1 MB: the copy engine may be busy with the tensor)
+    if (size_t(n) * sizeof(double) <= (1u << 20)) {
+      dev_upload(hF_.x[i][0], init + off, size_t(n) * sizeof(double), stream_);
+      NTF_CUDA(cudaMemcpyAsync(hF_.x[i][1], hF_.x[i][0], size_t(n) * sizeof(double), cudaMemcpyDeviceToDevice, stream_));
+    } else {
+      NTF_CUDA(cudaMemcpyAsync(hF_.x[i][0], init + off, size_t(n) * sizeof(double), cudaMemcpyHostToDevice, stream_));
+      NTF_CUDA(cudaMemcpyAsync(hF_.x[i][1], init + off, size_t(n) * sizeof(double), cudaMemcpyHostToDevice, stream_));
+    }
     off += n;
   }
-  NTF_CUDA(cudaMemcpyAsync(dF_.p, &hF_, sizeof hF_, cudaMemcpyHostToDevice, stream_));
+  dev_upload(dF_.p, &hF_, sizeof hF_, stream_);
 
   RunState st{};
   st.beta = params ? params->beta0 : 0.0;
@@ -510,7 +572,7 @@ Session::Session(ntf_ctx* ctx, const ntf_tensor* t, int algo, const double* init
   st.algo = algo;
   collective_time_ = ctx->comm.active() && cfg.max_time_s > 0.0;
   st.collective_time = collective_time_ ? 1 : 0;
-  NTF_CUDA(cudaMemcpyAsync(state_.p, &st, sizeof st, cudaMemcpyHostToDevice, stream_));
+  dev_upload(state_.p, &st, sizeof st, stream_);
 
   // GramCache::create + pivot objective f0 (driver_common.hpp:50-56), then
   // start the run clock (her.cpp:58 / ao.cpp:28). No host synchronisation:
@@ -786,5 +848,6 @@ ntf_tensor::~ntf_tensor() {
 }
 
 ntf_ctx::~ntf_ctx() {
+  if (setup) cudaStreamDestroy(setup);
   if (stream) cudaStreamDestroy(stream);
 }

@@ -230,6 +230,7 @@ struct ntf_ctx {
   int device = 0;
   int sms = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t setup = nullptr;  // table uploads of the engines (idle otherwise: never behind a tensor upload)
   ntfb::Comm comm;
   ntfb::DevBuf scratch;  // small shared scratch (norms, standalone NNLS)
   ~ntf_ctx();
