@@ -310,11 +310,9 @@ void run_driver(int algo, ntf_ctx* ctx, const ntf_tensor* t, const double* init,
       if (finished) break;
     }
   }
-  s.check_error();
-  s.factors(out_factors);
   std::vector<ntf_trace_record> recs(size_t(std::max(trace_cap, 0)));
   int n = 0;
-  s.trace(f0, recs.data(), trace_cap, &n);
+  s.finish(out_factors, f0, recs.data(), trace_cap, &n);
   *n_records = n;
   if (trace)
     for (int i = 0; i < std::min(n, trace_cap); ++i) {

@@ -811,6 +811,56 @@ bool Session::last_record(ntf_trace_record* out) {
   return true;
 }
 
+void Session::finish(double* out_factors, double* f0, ntf_trace_record* out, int cap, int* n) {
+  const int m0 = std::max(0, std::min(cap, trace_cap_));
+  if (m0 > 4096) {  // a long trace: its length first, then only the records that exist
+    check_error();
+    factors(out_factors);
+    trace(f0, out, cap, n);
+    return;
+  }
+  const size_t fac_bytes = size_t(2 * total_factor_len_) * sizeof(double);
+  const size_t tr_bytes = size_t(m0) * sizeof(TraceEntry);
+  const size_t off_state = (sizeof(DevFactors) + 63) / 64 * 64;
+  const size_t off_trace = off_state + (sizeof(RunState) + 63) / 64 * 64;
+  const size_t off_fac = off_trace + (tr_bytes + 63) / 64 * 64;
+  unsigned char* h = static_cast<unsigned char*>(ctx_->staging(off_fac + fac_bytes));
+  NTF_CUDA(cudaMemcpyAsync(h, dF_.p, sizeof(DevFactors), cudaMemcpyDeviceToHost, stream_));
+  NTF_CUDA(cudaMemcpyAsync(h + off_state, state_.p, sizeof(RunState), cudaMemcpyDeviceToHost, stream_));
+  if (tr_bytes) NTF_CUDA(cudaMemcpyAsync(h + off_trace, trace_.p, tr_bytes, cudaMemcpyDeviceToHost, stream_));
+  NTF_CUDA(cudaMemcpyAsync(h + off_fac, fac_.p, fac_bytes, cudaMemcpyDeviceToHost, stream_));
+  sync();
+  DevFactors hf;
+  RunState st;
+  std::memcpy(&hf, h, sizeof hf);
+  std::memcpy(&st, h + off_state, sizeof st);
+  if (st.error) throw std::runtime_error(solver_error_message(st.error));
+  const double* fac = reinterpret_cast<const double*>(h + off_fac);
+  long long off = 0;
+  for (int i = 0; i < order_; ++i) {  // x[i][b] = fac_ + 2 off + b n (the constructor's layout)
+    const long long nn = (long long)rows_[i] * rank_;
+    std::memcpy(out_factors + off, fac + 2 * off + (hf.sel[i] ? nn : 0), size_t(nn) * sizeof(double));
+    off += nn;
+  }
+  if (f0) *f0 = st.f0;
+  *n = st.k;
+  const TraceEntry* tr = reinterpret_cast<const TraceEntry*>(h + off_trace);
+  for (int i = 0; i < std::min(st.k, m0); ++i) {
+    ntf_trace_record r{};
+    r.iter = i + 1;
+    r.time_s = tr[i].time_s;
+    r.f = tr[i].f;
+    r.inner_sweeps = tr[i].sweeps;
+    if (algo_ == 0) {
+      r.has_restarted = 1;
+      r.restarted = tr[i].restarted;
+      r.has_beta = 1;
+      r.beta = tr[i].beta;
+    }
+    out[i] = r;
+  }
+}
+
 void Session::check_error() {
   int e = 0;
   NTF_CUDA(cudaMemcpyAsync(&e, &state_.as<RunState>()->error, sizeof(int), cudaMemcpyDeviceToHost, stream_));
@@ -847,7 +897,20 @@ ntf_tensor::~ntf_tensor() {
   if (ready) cudaEventDestroy(ready);
 }
 
+void* ntf_ctx::staging(size_t bytes) const {
+  if (bytes > pinned_bytes) {
+    if (pinned) cudaFreeHost(pinned);
+    pinned = nullptr;
+    pinned_bytes = 0;
+    const size_t want = std::max<size_t>(bytes, 1 << 20);
+    NTF_CUDA(cudaHostAlloc(&pinned, want, cudaHostAllocDefault));
+    pinned_bytes = want;
+  }
+  return pinned;
+}
+
 ntf_ctx::~ntf_ctx() {
+  if (pinned) cudaFreeHost(pinned);
   if (setup) cudaStreamDestroy(setup);
   if (stream) cudaStreamDestroy(stream);
 }

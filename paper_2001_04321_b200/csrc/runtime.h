@@ -177,6 +177,8 @@ class Session {
   void trace(double* f0, ntf_trace_record* out, int cap, int* n);
   bool last_record(ntf_trace_record* out);  // the newest trace record (false: none yet)
   void check_error();  // throws the inner solver's failure (std::runtime_error in the reference)
+  // error check + accepted factors + trace in one staged download (the drivers' epilogue)
+  void finish(double* out_factors, double* f0, ntf_trace_record* out, int cap, int* n);
   void set_kernel_timing(bool on);
   void kernel_times(double* ms_per_mode, int* launches, int* total_kernels);
   cudaStream_t stream() const { return stream_; }
@@ -231,6 +233,10 @@ struct ntf_ctx {
   int sms = 0;
   cudaStream_t stream = nullptr;
   cudaStream_t setup = nullptr;  // table uploads of the engines (idle otherwise: never behind a tensor upload)
+  // page-locked staging of a run's results (one download, one synchronisation); grows on demand
+  mutable void* pinned = nullptr;
+  mutable size_t pinned_bytes = 0;
+  void* staging(size_t bytes) const;
   ntfb::Comm comm;
   ntfb::DevBuf scratch;  // small shared scratch (norms, standalone NNLS)
   ~ntf_ctx();
