@@ -1,6 +1,6 @@
 #!/bin/bash
-# validation of the r02be state: full GPU suite, smoke, driver-style bench lines, C3/C4/C5, launch list
-O=gpurun_out/r02be; mkdir -p $O
+# validation of the r02bj state: full GPU suite, smoke, driver-style bench lines, C3/C4/C5, launch list
+O=gpurun_out/r02bj; mkdir -p $O
 timeout 3000 python -m pytest tests -m gpu -q > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?"
 timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > $O/smoke.log 2>&1; echo "smoke rc=$?"
 timeout 600 python bench.py --gpus 1 --steps 20 --warmup 5 > $O/bench_c2_k20.json 2> $O/bench_c2_k20.err; echo "bench k20 rc=$?"
@@ -13,7 +13,7 @@ timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
 tail -4 $O/pytest_gpu.log
 python - <<'PY'
 import json,glob
-for f in sorted(glob.glob("gpurun_out/r02be/bench_*.json")):
+for f in sorted(glob.glob("gpurun_out/r02bj/bench_*.json")):
     try:
         d=json.loads(open(f).read().strip().splitlines()[-1])
         print(f.split('/')[-1], round(d["value"],2), "e2e", round(d["e2e"]["value"],2), d.get("roofline",{}).get("per_mode_ms"), d.get("roofline",{}).get("frac"), d.get("roofline",{}).get("fma_frac"))
