@@ -365,6 +365,7 @@ def run_ours(args):
     except Exception:
         pass
     sess.close()
+    prov.close()  # the device-timed run's tensor goes back to the buffer pool before the e2e runs upload theirs
 
     # e2e through the public C-ABI driver with host buffers: upload of the
     # tensor (the provider), init, K iterations, factors + trace back to the
