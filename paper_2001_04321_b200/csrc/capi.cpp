@@ -289,15 +289,13 @@ void run_driver(int algo, ntf_ctx* ctx, const ntf_tensor* t, const double* init,
     std::vector<double> acc(static_cast<size_t>(len));
     while (true) {
       s.step(1);
-      s.sync();
-      const bool finished = s.done();
-      const int k = s.iterations();
-      if (cfg->record_factor_error || observer) s.factors(acc.data());
+      bool finished = false;
+      int k = 0;
+      ntf_trace_record last{};
+      s.snapshot(acc.data(), observer ? &last : nullptr, &k, &finished);  // one download, one synchronisation
       if (cfg->record_factor_error)
         e_values.push_back(factor_error(acc.data(), cfg->ground_truth, shape.data(), t->order, rank));
       if (observer) {
-        ntf_trace_record last{};
-        s.last_record(&last);
         ntf_her_iteration_info info{};
         info.iter = k;
         info.f_hat = last.f;

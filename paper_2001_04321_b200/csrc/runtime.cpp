@@ -811,6 +811,58 @@ bool Session::last_record(ntf_trace_record* out) {
   return true;
 }
 
+void Session::snapshot(double* factors_out, ntf_trace_record* last, int* k, bool* done) {
+  const size_t fac_bytes = factors_out ? size_t(2 * total_factor_len_) * sizeof(double) : 0;
+  const size_t off_state = (sizeof(DevFactors) + 63) / 64 * 64;
+  const size_t off_rec = off_state + (sizeof(RunState) + 63) / 64 * 64;
+  const size_t off_fac = off_rec + 64;
+  unsigned char* h = static_cast<unsigned char*>(ctx_->staging(off_fac + fac_bytes));
+  // the newest record is entry host_iters_ - 1 unless the run stopped earlier (then a second, rare, copy)
+  const int guess = std::min(host_iters_, trace_cap_) - 1;
+  NTF_CUDA(cudaMemcpyAsync(h, dF_.p, sizeof(DevFactors), cudaMemcpyDeviceToHost, stream_));
+  NTF_CUDA(cudaMemcpyAsync(h + off_state, state_.p, sizeof(RunState), cudaMemcpyDeviceToHost, stream_));
+  if (guess >= 0)
+    NTF_CUDA(cudaMemcpyAsync(h + off_rec, trace_.as<TraceEntry>() + guess, sizeof(TraceEntry), cudaMemcpyDeviceToHost, stream_));
+  if (fac_bytes) NTF_CUDA(cudaMemcpyAsync(h + off_fac, fac_.p, fac_bytes, cudaMemcpyDeviceToHost, stream_));
+  sync();
+  DevFactors hf;
+  RunState st;
+  std::memcpy(&hf, h, sizeof hf);
+  std::memcpy(&st, h + off_state, sizeof st);
+  *k = st.k;
+  *done = st.done != 0;
+  if (factors_out) {
+    const double* fac = reinterpret_cast<const double*>(h + off_fac);
+    long long off = 0;
+    for (int i = 0; i < order_; ++i) {
+      const long long nn = (long long)rows_[i] * rank_;
+      std::memcpy(factors_out + off, fac + 2 * off + (hf.sel[i] ? nn : 0), size_t(nn) * sizeof(double));
+      off += nn;
+    }
+  }
+  if (last && st.k >= 1 && st.k <= trace_cap_) {
+    TraceEntry e;
+    if (st.k - 1 == guess) {
+      std::memcpy(&e, h + off_rec, sizeof e);
+    } else {
+      NTF_CUDA(cudaMemcpyAsync(&e, trace_.as<TraceEntry>() + (st.k - 1), sizeof e, cudaMemcpyDeviceToHost, stream_));
+      sync();
+    }
+    ntf_trace_record r{};
+    r.iter = st.k;
+    r.time_s = e.time_s;
+    r.f = e.f;
+    r.inner_sweeps = e.sweeps;
+    if (algo_ == 0) {
+      r.has_restarted = 1;
+      r.restarted = e.restarted;
+      r.has_beta = 1;
+      r.beta = e.beta;
+    }
+    *last = r;
+  }
+}
+
 void Session::finish(double* out_factors, double* f0, ntf_trace_record* out, int cap, int* n) {
   const int m0 = std::max(0, std::min(cap, trace_cap_));
   if (m0 > 4096) {  // a long trace: its length first, then only the records that exist

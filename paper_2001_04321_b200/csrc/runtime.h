@@ -177,6 +177,9 @@ class Session {
   void trace(double* f0, ntf_trace_record* out, int cap, int* n);
   bool last_record(ntf_trace_record* out);  // the newest trace record (false: none yet)
   void check_error();  // throws the inner solver's failure (std::runtime_error in the reference)
+  // after an iteration of an observed run: done flag, iteration count, the newest trace record and
+  // (factors_out != null) the accepted factors, in one staged download and one synchronisation
+  void snapshot(double* factors_out, ntf_trace_record* last, int* k, bool* done);
   // error check + accepted factors + trace in one staged download (the drivers' epilogue)
   void finish(double* out_factors, double* f0, ntf_trace_record* out, int cap, int* n);
   void set_kernel_timing(bool on);
