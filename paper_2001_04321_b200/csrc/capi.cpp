@@ -99,7 +99,9 @@ void check_run_inputs(const ntf_tensor* t, const double* init, int rank, const n
   // any factor height (taller than one cluster: the grid-kernel path of
   // kernels_nnls_tall.cu); the other inner solvers keep a factor on one
   // thread-block cluster
-  if (rank > kMaxRank) throw Unsupported("rank above the NNLS kernels' limit (64)");
+  if (rank > kMaxTallRank) throw Unsupported("rank above the NNLS kernels' limit (128)");
+  if (cfg.solver != NTF_SOLVER_AHALS && rank > kMaxRank)
+    throw Unsupported("the PGD / Nesterov / ADMM / active-set kernels serve ranks up to 64 (AHALS: 128)");
   if (cfg.solver != NTF_SOLVER_AHALS)
     for (int i = 0; i < t->order; ++i)
       if (t->shape[i] > kMaxNnlsRows)

@@ -1506,12 +1506,12 @@ bool nnls_needs_tall(int rows, int rank) {
     const char* e = std::getenv("NTF_NNLS_TALL");
     return e && std::atoi(e) != 0;
   }();
-  return force || rows > kMaxNnlsRows || (rank > 32 && rows > 2048);
+  return force || rows > kMaxNnlsRows || (rank > 32 && rows > 2048) || rank > kMaxRank;
 }
 
 void launch_nnls(const NnlsLaunch& a, cudaStream_t s) {
   const int r = a.rank;
-  if (r < 1 || r > kMaxRank) throw Unsupported("rank outside the fused NNLS kernel's range (1..64)");
+  if (r < 1 || r > kMaxTallRank) throw Unsupported("rank outside the NNLS kernels' range (1..128)");
   if (nnls_needs_tall(a.rows, r)) {
     if (!a.tall) throw Unsupported("factor taller than one cluster holds and no tall-path workspace");
     return launch_nnls_tall(a, s, a.zero_sweeps ? 0 : a.max_iters);

@@ -1,5 +1,6 @@
 // Fused block update for factors too tall for one thread-block cluster
-// (I_n > 4096, or beyond the fused kernels' per-rank row limits).
+// (I_n > 4096, or beyond the fused kernels' per-rank row limits) or ranks
+// above the fused kernels' 64 (up to 128).
 //
 // The fused kernels (kernels_nnls.cu) keep a whole factor on one 16-CTA
 // cluster; the reference has no height limit (nnls.cpp:15-49 loops over all
@@ -39,7 +40,7 @@ constexpr int kGramRowsPerBlock = 1024;
 
 struct TallCtl {
   int stopped, sweeps, skip, max_iters;  // skip: the run's budget is exhausted (whole update is a no-op)
-  unsigned long long okbits;             // columns updated (G_jj above the floor)
+  unsigned long long okbits[2];          // columns updated (G_jj above the floor), r <= 128
   double tol, first, beta;
   unsigned counter;
 };
@@ -125,11 +126,12 @@ __global__ void tall_setup_kernel(NnlsLaunch a, double* ws) {
   __syncthreads();
   if (threadIdx.x == 0) {
     const double floor_ = 1e-12 * dmax_s;  // nnls.cpp:16-19
-    unsigned long long ok = 0;
+    unsigned long long ok[2] = {0, 0};
     for (int j = 0; j < r; ++j)
-      if (w.G[j * r + j] > floor_) ok |= 1ull << j;
+      if (w.G[j * r + j] > floor_) ok[j >> 6] |= 1ull << (j & 63);
     TallCtl c{};
-    c.okbits = ok;
+    c.okbits[0] = ok[0];
+    c.okbits[1] = ok[1];
     c.skip = 0;
     if (a.F) {
       c.max_iters = a.zero_sweeps ? 0 : a.st->inner_max_iters;
@@ -169,16 +171,16 @@ __global__ void __launch_bounds__(kTallThreads) tall_sweep_kernel(NnlsLaunch a, 
   if (ctl->skip || ctl->stopped || s >= ctl->max_iters) return;  // uniform over the grid (set by earlier launches)
   for (int e = threadIdx.x; e < r * r; e += blockDim.x) Gs[e] = w.G[e];
   __syncthreads();
-  const unsigned long long ok = ctl->okbits;
+  const unsigned long long ok[2] = {ctl->okbits[0], ctl->okbits[1]};
   const int row = blockIdx.x * blockDim.x + threadIdx.x;
   double d2 = 0.0;
   if (row < a.rows) {
-    double x[kMaxRank];
+    double x[kMaxTallRank];
     double* wr = w.W + (long long)row * r;
     const double* cr = a.C + (long long)row * r;
     for (int l = 0; l < r; ++l) x[l] = wr[l];
     for (int j = 0; j < r; ++j) {
-      if (!((ok >> j) & 1)) continue;
+      if (!((ok[j >> 6] >> (j & 63)) & 1)) continue;
       const double gjj = Gs[j * r + j];
       double acc = 0.0;  // W_{i,:} G_{:,j} with the latest entries
       for (int l = 0; l < r; ++l) acc = fma(x[l], Gs[l * r + j], acc);
@@ -365,7 +367,7 @@ size_t nnls_tall_workspace(int rows, int rank) {
 // max_iters_host: the inner sweep budget as the host knows it (the launch count of the sweep kernel)
 void launch_nnls_tall(const NnlsLaunch& a, cudaStream_t s, int max_iters_host) {
   if (!a.tall) throw LogicError("tall NNLS path without a workspace");
-  if (a.rank > kMaxRank) throw Unsupported("rank outside the NNLS kernels' range (1..64)");
+  if (a.rank > kMaxTallRank) throw Unsupported("rank outside the NNLS kernels' range (1..128)");
   double* ws = a.tall;
   const int nb = (a.rows + kTallThreads - 1) / kTallThreads;
   const int ng = (a.rows + kGramRowsPerBlock - 1) / kGramRowsPerBlock;
@@ -373,6 +375,8 @@ void launch_nnls_tall(const NnlsLaunch& a, cudaStream_t s, int max_iters_host) {
   tall_setup_kernel<<<1, 256, 0, s>>>(a, ws);
   tall_init_kernel<<<std::min(nb, 1024), kTallThreads, 0, s>>>(a, ws);
   const size_t smem = size_t(a.rank) * a.rank * sizeof(double);
+  if (smem > 48 * 1024)
+    NTF_CUDA(cudaFuncSetAttribute(tall_sweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   for (int it = 0; it < max_iters_host; ++it) tall_sweep_kernel<<<nb, kTallThreads, smem, s>>>(a, ws, it);
   tall_epilogue_kernel<<<nb, kTallThreads, 0, s>>>(a, ws);
   if (a.role != 2) {

@@ -34,7 +34,8 @@ struct NvtxRange {
 namespace ntfb {
 
 constexpr int kMaxOrder = NTF_MAX_ORDER;
-constexpr int kMaxRank = 64;  // largest r served by the fused NNLS kernel
+constexpr int kMaxRank = 64;  // largest r served by the fused NNLS kernels
+constexpr int kMaxTallRank = 128;  // largest r of the grid-kernel block update (kernels_nnls_tall.cu)
 constexpr int kMaxNnlsRows = 16 * 256;  // largest factor height it serves (one 16-CTA cluster)
 constexpr int kNnlsReserveSms = 16;      // SMs a concurrent pass leaves to the NNLS cluster
 

@@ -336,6 +336,35 @@ def test_tall_standalone_ahals_and_solver_limits(P, oracle):
         P.her_run(t, init, P.AoConfig(max_outer_iters=2, solver=P.NnlsSolver.pgd))
 
 
+@pytest.mark.parametrize("shape,rank", [([40, 30, 20], 100), ([60, 20, 12], 128), ([12, 10, 9, 8], 72)])
+def test_ranks_above_the_fused_kernels_limit(P, oracle, shape, rank):
+    """The reference has no rank limit. Ranks above 64 (the fused kernels'
+    register budget) run the generic MTTKRP and the grid-kernel block update,
+    up to r = 128: per-call MTTKRP, HER trace and standalone AHALS against
+    the oracle; r = 129 and the other inner solvers above 64 are refused."""
+    t, truth, init = _instance(P, shape, rank, 0.01, 5)
+    prov = P.GpuDenseProvider(t)
+    for mode in range(len(shape)):
+        assert rel_fro(prov.mttkrp(init, mode), oracle.mttkrp(np.asarray(t), init.factors, mode)) < 1e-12
+    model, trace = P.her_run(prov, init, P.AoConfig(max_outer_iters=8), P.HerParams())
+    prov.close()
+    fo, f0, recs = oracle.run("her", t, init.factors, max_outer_iters=8)
+    compare_traces(trace, f0, recs, oracle.norm_sq(t), n_check=8)
+    gen = np.random.default_rng(rank)
+    b = gen.random((400, rank))
+    g = b.T @ b
+    c = gen.random((90, rank)) * rank
+    w0 = gen.random((90, rank))
+    want, sweeps = oracle.ahals_solve(g, c, w0, 20, 1e-3, return_sweeps=True)
+    got, got_sweeps = P.ahals_solve(g, c, w0, P.InnerStop(20, 1e-3), return_sweeps=True)
+    assert got_sweeps == sweeps and rel_fro(got, want) < 1e-11
+    t2, _, init2 = _instance(P, [6, 5, 4], 129, 0.0, 1)
+    with pytest.raises(P.UnsupportedError, match="128"):
+        P.her_run(t2, init2, P.AoConfig(max_outer_iters=2))
+    with pytest.raises(P.UnsupportedError, match="64"):
+        P.her_run(t, init, P.AoConfig(max_outer_iters=2, solver=P.NnlsSolver.admm))
+
+
 def test_tall_path_forced_on_small_instances_matches_the_fused_kernels():
     """NTF_NNLS_TALL=1 routes every block update through the grid-kernel path:
     the trace and AHALS parity tests of this module, re-run that way in a
